@@ -1,0 +1,158 @@
+// engine.hpp — internal interface between the host library (C++20) and the
+// device engine (CUDA, sm_100a).  No CUDA types appear here so the host
+// sources compile with plain g++.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace ssb {
+
+enum PopKind : int { kIzhikevich = 0, kPoisson = 1, kCondLif = 2 };
+
+// One population, compiled for the device: constants already cast to the
+// storage precision exactly as Simulation's constructor does
+// (reference engine.cpp:163-210).
+struct HostPop {
+    std::string name;
+    int kind = kCondLif;
+    int n = 0;
+    // CondLif constants (fp32, engine.cpp:192-198)
+    float tauM = 0, eLeak = 0, eExc = 0, eInh = 0, vThresh = 0, vReset = 0, synDecay = 0;
+    // Poisson (engine.cpp:186): p in fp64
+    double p = 0.0;
+    // Izhikevich per-neuron parameters (fp32) and drives (fp64)
+    std::vector<float> a, b, c, d;
+    std::vector<double> noise, bias;
+    // RNG stream ("<name>/source" or "<name>/noise"): MT19937-64 state
+    std::array<std::uint64_t, 312> mt{};
+    int mtPos = 312;
+};
+
+// One synapse group after gen_fixed_outdegree, gScale and StorageMode.
+struct HostGroup {
+    std::string name;
+    int pre = 0, post = 0;
+    int preOffset = 0, preCount = 0;
+    bool inhibitory = false;
+    bool dense = false;
+    int nPre = 0, nPost = 0;
+    int outDegree = 0;
+    // non-owning views of the host matrices (kept by the caller)
+    const float* W = nullptr;              // dense [nPre*nPost]
+    const float* g = nullptr;              // CRS gValues [nnz]
+    const std::int32_t* ind = nullptr;     // CRS postInd [nnz]
+    const std::int64_t* rowStart = nullptr;  // CRS [nPre+1]
+    std::int64_t nnz = 0;
+};
+
+struct HostNet {
+    std::vector<HostPop> pops;
+    std::vector<HostGroup> groups;
+    float dtS = 0.f;
+    double dtMs = 0.0;
+    double durationMs = 0.0;
+    std::int64_t steps = 0;
+};
+
+struct EngineConfig {
+    int device = 0;
+    int window = 64;
+    int blockSize = 0;
+    int blockPolicy = 0;
+    bool useGraphs = true;
+    int heavyPreThreshold = 1024;
+    std::int64_t rasterCapacity = 0;  // 0 = automatic
+    bool profile = false;
+    bool forceStepMode = false;
+};
+
+struct KernelStat {
+    std::string name;
+    std::int64_t launches = 0;
+    double totalMs = 0.0;
+    double bytes = 0.0;
+};
+
+enum StateField : int {
+    kFieldV = 0, kFieldU, kFieldGExc, kFieldGInh, kFieldExcIn, kFieldInhIn, kFieldNanFlag,
+    kFieldFlagged
+};
+
+// Thrown for CUDA failures (maps to SSB_ERR_INTERNAL).
+struct DeviceError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+class DeviceEngine {
+public:
+    DeviceEngine(const HostNet& net, const EngineConfig& cfg);
+    ~DeviceEngine();
+    DeviceEngine(const DeviceEngine&) = delete;
+    DeviceEngine& operator=(const DeviceEngine&) = delete;
+
+    // Advances n steps (n <= steps remaining; checked by the caller).
+    void step(std::int64_t n);
+    void sync();
+    std::int64_t steps_done() const;
+
+    // State access (count elements; FLAGGED is one int64).
+    void pull(int pop, int field, void* dst, std::int64_t count);
+    void push(int pop, int field, const void* src, std::int64_t count);
+
+    // Raster: flushes device events to the host store and returns it.
+    // counts: [steps_done * nPops] spikes per (step, pop); neurons: ids in
+    // (step, pop, neuron) order.
+    void collect_raster(std::vector<std::int32_t>& counts, std::vector<std::int32_t>& neurons);
+    void discard_raster();
+    void spike_totals(std::vector<std::int64_t>& perPop);
+
+    void* stream() const;
+    int window() const;
+    int block_size(int pop) const;
+    bool step_mode() const;
+    std::int64_t device_bytes() const;
+    std::vector<KernelStat> kernel_stats();
+    void reset_kernel_stats();
+
+    struct Impl;
+
+private:
+    std::unique_ptr<Impl> impl_;
+};
+
+// Standalone kernels over caller host arrays (reference propagate /
+// detect_nans, engine.cpp:27-80).  Throw DeviceError on CUDA failure.
+void device_propagate_dense(const float* w, int nPre, int nPost, const std::int32_t* spikes,
+                            std::int64_t nSpikes, float* acc);
+void device_propagate_crs(const float* g, const std::int32_t* ind, const std::int64_t* rowStart,
+                          int nPre, int nPost, const std::int32_t* spikes, std::int64_t nSpikes,
+                          float* acc);
+std::int64_t device_detect_nans(int kind, const float* v, const float* u, const float* gExc,
+                                const float* gInh, std::uint8_t* flag, std::int64_t n);
+
+// Device-pointer entry points (bench / kernel-level sweeps).
+void device_propagate_dense_dev(const float* w, int nPre, int nPost, const std::int32_t* spikes,
+                                int nSpikes, float* acc, void* stream);
+void device_crs_segments_dev(const std::int32_t* ind, const std::int64_t* rowStart, int nPre,
+                             int nPost, int tile, std::int32_t* seg, void* stream);
+void device_propagate_crs_dev(const float* g, const std::int32_t* ind, const std::int32_t* seg,
+                              int tile, int nPre, int nPost, const std::int32_t* spikes,
+                              int nSpikes, float* acc, void* stream);
+
+int device_count();
+struct DeviceProps {
+    std::string name;
+    int smCount = 0, warpSize = 32, maxThreadsPerSM = 0, maxBlocksPerSM = 0,
+        maxThreadsPerBlock = 0, regsPerSM = 0;
+    std::int64_t sharedPerSM = 0, sharedPerBlockOptin = 0;
+};
+DeviceProps device_props(int device);
+// numRegs / static shared bytes / max threads of an engine kernel by name.
+bool kernel_attributes(const std::string& name, int& regs, int& sharedBytes, int& maxThreads);
+
+}  // namespace ssb

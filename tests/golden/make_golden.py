@@ -1,0 +1,119 @@
+"""Generates the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container (it needs oracle/_ref/libsynscale_ref.so, which is
+compiled from /root/reference/proj by oracle/Makefile):
+
+    python tests/golden/make_golden.py
+
+Everything recorded here comes out of the unmodified reference library
+through its public C++ API (Simulation / gen_fixed_outdegree / RandomStream /
+derive_seed, via oracle/ref_shim.cpp).  The fixtures pin the oracle
+restatement and the CUDA path on machines where /root/reference is absent.
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+from oracle import oracle as O  # noqa: E402
+from paper_1412_0595_b200 import synscale as S  # noqa: E402
+import specs  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+STREAMS = [(7, 1, "pn/source"), (11, 1, "drive/source"), (11, 2, "damp/source"),
+           (42, 7, "pop/noise"), (0, 0, "gen/targets")]
+SEEDS = [(7, "pn_kc"), (7, "pn_lhi"), (7, "lhi_kc"), (7, "kc_dn"), (9, "exc"), (9, "inh")]
+GENS = [  # nPre, nPost, k, kind, lo, hi, value, sign, seed
+    (5, 8, 3, S.L.WEIGHT_UNIFORM, 0.0, 0.5, 0.0, 1, 99),
+    (3, 4, 2, S.L.WEIGHT_CONSTANT, 0.0, 0.0, 2.0, -1, 7),
+    (50, 80, 13, S.L.WEIGHT_UNIFORM, 0.0, 0.5, 0.0, 1, 99),
+    (100, 1000, 500, S.L.WEIGHT_UNIFORM, 0.0, 0.02, 0.0, 1, 2921146032820891623),
+]
+
+
+def run_ref(spec, mode):
+    d = S.NetDesc(spec)
+    sim = O.CpuSim(d.ptr, spec, int(mode), ref=True)
+    step, pop, neu = sim.finish()
+    out = {
+        "n_events": int(step.size),
+        "raster_sha": specs.sha(step, pop, neu),
+        "rates": [float(x) for x in sim.rates()],
+        "sum_nans": sim.sum_nans(),
+        "counts": [int(np.count_nonzero(pop == i)) for i in range(len(spec.populations))],
+        "state_sha": {},
+        "groups": {},
+        "head": [[int(a), int(b), int(c)] for a, b, c in zip(step[:40], pop[:40], neu[:40])],
+    }
+    for pi, p in enumerate(spec.populations):
+        out["state_sha"][p.name] = {f: specs.sha(sim.state(pi, f)) for f in
+                                    ("v", "gExc", "gInh", "excIn", "inhIn", "nanFlag")}
+    for gi, g in enumerate(spec.synapses):
+        kind, m = sim.group(gi)
+        out["groups"][g.name] = [kind, specs.sha(*(m if kind == "sparse" else (m,)))]
+    return out
+
+
+def main():
+    if not O.have_ref():
+        O.build()
+    gold = {"source": "reference (oracle/_ref/libsynscale_ref.so from /root/reference/proj)"}
+    gold["streams"] = {f"{g}/{e}/{lab}": [str(int(x)) for x in O.stream_u64(g, e, lab, 16, ref=True)]
+                       for g, e, lab in STREAMS}
+    gold["derive_seed"] = {f"{p}/{lab}": str(int(O.ref_lib().ref_derive_seed(p, lab.encode())))
+                           for p, lab in SEEDS}
+    gens = []
+    for args in GENS:
+        m = O.gen_fixed_outdegree(*args, ref=True)
+        entry = {"args": [str(a) if isinstance(a, int) and a > 2**31 else a for a in args],
+                 "sha": specs.sha(m), "nnz": int(np.count_nonzero(m))}
+        if m.size <= 64:
+            entry["weights"] = m.ravel().view(np.uint32).tolist()
+        gens.append(entry)
+    gold["gen_fixed_outdegree"] = gens
+
+    runs = {}
+    for name, (spec, mode) in {
+        "cfg1_1000ms": specs.config_spec(1, 1000.0),
+        "cfg2_100ms": specs.config_spec(2, 100.0),
+        "cfg3_20ms": specs.config_spec(3, 20.0),
+        "cfg1_sparse_300ms": (specs.config_spec(1, 300.0)[0], S.StorageMode.ForceSparse),
+        "cfg2_fromspec_100ms": (specs.config_spec(2, 100.0)[0], S.StorageMode.FromSpec),
+        "chain_100ms": (specs.chain_spec(100.0), S.StorageMode.FromSpec),
+        "recurrent_200ms": (specs.recurrent_lif_spec(), S.StorageMode.FromSpec),
+    }.items():
+        print("reference run", name, flush=True)
+        runs[name] = run_ref(spec, mode)
+    gold["runs"] = runs
+
+    # CondLif + Poisson known-answer network (test_engine.cpp:183-290): the
+    # reference's per-step v / gExc / gInh of the single conductance neuron.
+    kat = specs.condlif_kat_spec()
+    d = S.NetDesc(kat)
+    sim = O.CpuSim(d.ptr, kat, 0, ref=True)
+    v, ge, gi = [], [], []
+    for _ in range(sim.steps_total()):
+        sim.step(1)
+        v.append(sim.state(2, "v")[0])
+        ge.append(sim.state(2, "gExc")[0])
+        gi.append(sim.state(2, "gInh")[0])
+    step, pop, neu = sim.finish()
+    np.savez_compressed(os.path.join(OUT, "condlif_kat.npz"), v=np.array(v, np.float32),
+                        gExc=np.array(ge, np.float32), gInh=np.array(gi, np.float32),
+                        step=step, pop=pop, neuron=neu)
+
+    with open(os.path.join(OUT, "golden.json"), "w") as f:
+        json.dump(gold, f, indent=1, sort_keys=True)
+    print("wrote", os.path.join(OUT, "golden.json"))
+
+
+if __name__ == "__main__":
+    main()

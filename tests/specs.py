@@ -1,0 +1,122 @@
+"""Network specs shared by the tests, the golden generator, smoke() and bench.py.
+
+The mushroom-body configs follow SURVEY.md §8(d) / BASELINE.md §2:
+build_mbody_net(nPN=100, nLHI=20, nKC, nDN=100, seed=7) with dtMs=0.1,
+pnRateHz=50 and gScales pn_lhi=1.0, lhi_kc=0.1, pn_kc=0.5/frac, kc_dn=30/nKC.
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+from paper_1412_0595_b200 import synscale as S
+
+# BASELINE.json configs -> (nKC, pnKcOutFraction, storage mode)
+CONFIGS = {
+    1: (1_000, 0.5, S.StorageMode.ForceDense),
+    2: (10_000, 0.05, S.StorageMode.ForceSparse),
+    3: (100_000, 0.05, S.StorageMode.FromSpec),
+    4: (1_000_000, 0.05, S.StorageMode.FromSpec),
+}
+
+
+def mbody_gscales(n_kc: int, frac: float) -> dict:
+    return {"pn_kc": 0.5 / frac, "pn_lhi": 1.0, "lhi_kc": 0.1, "kc_dn": 30.0 / n_kc}
+
+
+def mbody_spec(n_kc: int, frac: float, duration_ms: float, dt_ms: float = 0.1, seed: int = 7,
+               n_pn: int = 100, n_lhi: int = 20, n_dn: int = 100) -> S.NetworkSpec:
+    opt = S.MBodyBuildOptions(dtMs=dt_ms, durationMs=duration_ms, pnKcOutFraction=frac)
+    return S.build_mbody_net(n_pn, n_lhi, n_kc, n_dn, mbody_gscales(n_kc, frac), seed, opt)
+
+
+def config_spec(cfg: int, duration_ms: float):
+    n_kc, frac, mode = CONFIGS[cfg]
+    return mbody_spec(n_kc, frac, duration_ms), mode
+
+
+def condlif_kat_spec() -> S.NetworkSpec:
+    """The conductance-neuron known-answer network of test_engine.cpp:183-238."""
+    spec = S.NetworkSpec(dtMs=1.0, durationMs=400.0, globalSeed=11)
+    spec.populations = [
+        S.NeuronPopulation("drive", 1, S.ModelKind.PoissonSource, 1, S.PoissonParams(200.0)),
+        S.NeuronPopulation("damp", 1, S.ModelKind.PoissonSource, 2, S.PoissonParams(80.0)),
+        S.NeuronPopulation("cell", 1, S.ModelKind.CondLif, 3, S.CondLifParams()),
+    ]
+    spec.synapses = [
+        S.SynapseGroupSpec("exc", "drive", "cell", S.SynapseSign.Excitatory, 1,
+                           S.WeightDist.constant(0.05)),
+        S.SynapseGroupSpec("inh", "damp", "cell", S.SynapseSign.Inhibitory, 1,
+                           S.WeightDist.constant(0.03)),
+    ]
+    return spec
+
+
+def recurrent_lif_spec(n: int = 200, duration_ms: float = 200.0, seed: int = 3) -> S.NetworkSpec:
+    """A CondLif population with self-connections (cyclic graph: one step per launch),
+    driven by Poisson input through a sparse group; exercises windows of 1."""
+    spec = S.NetworkSpec(dtMs=0.5, durationMs=duration_ms, globalSeed=seed)
+    spec.populations = [
+        S.NeuronPopulation("src", 50, S.ModelKind.PoissonSource, 1, S.PoissonParams(80.0)),
+        S.NeuronPopulation("net", n, S.ModelKind.CondLif, 2, S.CondLifParams()),
+    ]
+    spec.synapses = [
+        S.SynapseGroupSpec("drive", "src", "net", S.SynapseSign.Excitatory, n // 4,
+                           S.WeightDist.uniform(0.0, 0.4), 1.0, S.StorageKind.Sparse),
+        S.SynapseGroupSpec("rec_e", "net", "net", S.SynapseSign.Excitatory, n // 10,
+                           S.WeightDist.uniform(0.0, 0.05), 1.0, S.StorageKind.Dense, 0, n // 2),
+        S.SynapseGroupSpec("rec_i", "net", "net", S.SynapseSign.Inhibitory, n // 10,
+                           S.WeightDist.uniform(0.0, 0.08), 1.0, S.StorageKind.Sparse, n // 2, -1),
+    ]
+    return spec
+
+
+def chain_spec(duration_ms: float = 100.0) -> S.NetworkSpec:
+    """Feed-forward chain with two groups on one accumulator (fold order across
+    groups), a windowed pre range, a Poisson target and mixed storage."""
+    spec = S.NetworkSpec(dtMs=0.25, durationMs=duration_ms, globalSeed=19)
+    spec.populations = [
+        S.NeuronPopulation("in_a", 64, S.ModelKind.PoissonSource, 1, S.PoissonParams(120.0)),
+        S.NeuronPopulation("in_b", 300, S.ModelKind.PoissonSource, 2, S.PoissonParams(40.0)),
+        S.NeuronPopulation("mid", 700, S.ModelKind.CondLif, 3, S.CondLifParams()),
+        S.NeuronPopulation("out", 90, S.ModelKind.CondLif, 4,
+                           S.CondLifParams(tauMMs=8.0, tauSynMs=3.0)),
+        S.NeuronPopulation("sink", 40, S.ModelKind.PoissonSource, 5, S.PoissonParams(5.0)),
+    ]
+    spec.synapses = [
+        S.SynapseGroupSpec("a_mid", "in_a", "mid", S.SynapseSign.Excitatory, 200,
+                           S.WeightDist.uniform(0.0, 0.05), 2.0, S.StorageKind.Sparse),
+        S.SynapseGroupSpec("b_mid", "in_b", "mid", S.SynapseSign.Excitatory, 120,
+                           S.WeightDist.uniform(0.01, 0.03), 1.5, S.StorageKind.Dense, 20, 250),
+        S.SynapseGroupSpec("a_mid_i", "in_a", "mid", S.SynapseSign.Inhibitory, 50,
+                           S.WeightDist.constant(0.02), 1.0, S.StorageKind.Dense),
+        S.SynapseGroupSpec("mid_out", "mid", "out", S.SynapseSign.Excitatory, 30,
+                           S.WeightDist.uniform(0.0, 0.01), 3.0, S.StorageKind.Sparse),
+        S.SynapseGroupSpec("mid_out2", "mid", "out", S.SynapseSign.Excitatory, 90,
+                           S.WeightDist.constant(0.002), 1.0, S.StorageKind.Dense),
+        S.SynapseGroupSpec("out_sink", "out", "sink", S.SynapseSign.Inhibitory, 10,
+                           S.WeightDist.constant(0.5), 1.0, S.StorageKind.Sparse),
+    ]
+    return spec
+
+
+def sha(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def bits_equal(a: np.ndarray, b: np.ndarray) -> bool:
+    """Bitwise equality of float arrays, any NaN equal to any NaN."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    if a.shape != b.shape:
+        return False
+    if a.dtype.kind != "f":
+        return bool(np.array_equal(a, b))
+    na, nb = np.isnan(a), np.isnan(b)
+    if not np.array_equal(na, nb):
+        return False
+    return bool(np.array_equal(a[~na].view(np.uint32), b[~nb].view(np.uint32)))
