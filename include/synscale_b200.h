@@ -295,6 +295,8 @@ SSB_API int ssb_kernel_stats(ssb_sim* sim, ssb_kernel_stat* out, int32_t n);
 SSB_API int ssb_kernel_stats_reset(ssb_sim* sim);
 /* Device bytes held by the handle. */
 SSB_API int64_t ssb_device_bytes(const ssb_sim* sim);
+/* Kernel launches issued by ssb_step so far (graph nodes count individually). */
+SSB_API int64_t ssb_kernel_launches(const ssb_sim* sim);
 
 /* ---- occupancy model (occupancy.cpp) -------------------------------------- */
 SSB_API int ssb_device_preset(const char* name, ssb_device_spec* out, char* err, size_t errlen);

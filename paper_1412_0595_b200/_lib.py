@@ -161,6 +161,7 @@ _SIGNATURES = {
     "ssb_kernel_stats": (C.c_int, [_vp, P(ssb_kernel_stat), _i32]),
     "ssb_kernel_stats_reset": (C.c_int, [_vp]),
     "ssb_device_bytes": (_i64, [_vp]),
+    "ssb_kernel_launches": (_i64, [_vp]),
     "ssb_device_preset": (C.c_int, [_cp, P(ssb_device_spec), _cp, _sz]),
     "ssb_device_preset_names": (_cp, []),
     "ssb_device_query": (C.c_int, [_i32, P(ssb_device_spec), _cp, _sz]),

@@ -3,7 +3,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <numeric>
 #include <string>
@@ -58,6 +60,8 @@ bool kernel_attributes(const std::string& name, int& regs, int& sharedBytes, int
     if (name == "condlif_window") e = cudaFuncGetAttributes(&a, ssbk::condlif_window_kernel);
     else if (name == "poisson_window") e = cudaFuncGetAttributes(&a, ssbk::poisson_window_kernel);
     else if (name == "dense_window") e = cudaFuncGetAttributes(&a, ssbk::dense_window_kernel);
+    else if (name == "dense_window_tma")
+        e = cudaFuncGetAttributes(&a, ssbk::dense_window_tma_kernel);
     else if (name == "sparse_window") e = cudaFuncGetAttributes(&a, ssbk::sparse_window_kernel);
     else if (name == "compact_window") e = cudaFuncGetAttributes(&a, ssbk::compact_window_kernel);
     else if (name == "raster_window") e = cudaFuncGetAttributes(&a, ssbk::raster_window_kernel);
@@ -83,6 +87,12 @@ struct DeviceEngine::Impl {
         bool sparseInline = false;  // needs a dynamic shared tile
         ssbk::PopDev dev{};
         ssbk::AccDev acc[2]{};
+        ssbk::StageAcc stage[2]{};  // shared-memory staging plan (condlif)
+        int smemBytes = 0;          // dynamic shared memory of the population kernel
+        int offBits = -1;           // shared copy of the window's spike bits (1-block pops)
+        int tileN = 0;              // neurons per block
+        int chunk = 1;              // steps per phase-A/phase-B chunk
+        int offIn = 0;              // shared offset of the phase-A inputs
         std::vector<int> accGroups[2];  // group indices in spec order
         std::string name;
     };
@@ -108,10 +118,17 @@ struct DeviceEngine::Impl {
     std::int64_t stepsDone = 0;
     std::int64_t windowsLaunched = 0;
 
-    // raster
+    // raster: the device arena is flushed to the host only when it may be
+    // near full.  The cursor after each window is copied asynchronously to a
+    // pinned ring; the host never runs more than kRing windows ahead, so the
+    // arena fill is known up to kRing windows of worst-case growth.
+    static constexpr int kRing = 4;
     ssbk::RasterDev raster{};
     std::int64_t rasterCap = 0;
-    std::int64_t eventBound = 0;  // upper bound of events in the arena
+    long long* ringVal = nullptr;  // pinned
+    cudaEvent_t ringEv[kRing] = {};
+    std::int64_t ringAdd[kRing] = {};
+    std::int64_t knownCursor = 0, knownWin = 0, epochStart = 0;
     std::vector<std::int32_t> hostNeurons;
     bool rasterDiscarded = false;
 
@@ -150,8 +167,13 @@ struct DeviceEngine::Impl {
         return e;
     }
 
+    std::int64_t kernelLaunches = 0;  // kernels of this engine launched so far
+    int enqueued = 0;                 // kernels put on the stream by enqueue_window
+    std::map<int, int> kernelsPerWindow;
+
     template <typename F>
     void launch(const std::string& name, F&& f) {
+        ++enqueued;
         if (!cfg.profile) {
             f();
             CK(cudaGetLastError());
@@ -181,44 +203,157 @@ struct DeviceEngine::Impl {
         pending.clear();
     }
 
-    int choose_block(int n, bool sparseInline) const;
+    int choose_block(int n, const std::function<std::int64_t(int)>& smemFor,
+                     const void* kernelFn) const;
+    int plan_stage(const HostNet& net, int pi, int tileN, ssbk::StageAcc out[2], int& offIn,
+                   int& C, int& offBits) const;
     void build(const HostNet& net);
     void enqueue_window(int W);
     void run_window(int W);
     void flush_raster();
+
+    static constexpr int kRowBlock = 128;
+    static int ring_smem(int bd, bool tma) {
+        return ssbk::kRingStages * ssbk::kRingRows * bd * 4 + (tma ? ssbk::kRingStages * 8 : 0) +
+               ssbk::kListSeg * 4;
+    }
+    // Dense group inputs for window steps [wLo, wLo + nW): spiking rows
+    // streamed through shared memory (cp.async by default, TMA bulk copies
+    // with SSB_DENSE_KERNEL=tma) when they are 16-byte multiples, plain
+    // coalesced gathers otherwise.
+    bool useTma = false;
+    void launch_dense(const ssbk::GroupDev& G, const std::string& gname, const char* tag,
+                      float* out, long long stride, int wLo, int nW, int first) {
+        if (G.nPost % 4 == 0 && !useTma) {
+            dim3 grid((G.nPost + kRowBlock - 1) / kRowBlock, nW);
+            launch(std::string(tag) + gname, [&] {
+                ssbk::dense_window_pipe_kernel<<<grid, kRowBlock, ring_smem(kRowBlock, false),
+                                                 stream>>>(G, out, stride, wLo, first);
+            });
+        } else if (G.nPost % 4 == 0) {
+            dim3 grid((G.nPost + kRowBlock - 1) / kRowBlock, nW);
+            launch(std::string(tag) + gname, [&] {
+                ssbk::dense_window_tma_kernel<<<grid, kRowBlock, ring_smem(kRowBlock, true),
+                                                stream>>>(G, out, stride, wLo, first);
+            });
+        } else {
+            dim3 grid((G.nPost + 127) / 128, nW);
+            launch(std::string(tag) + gname, [&] {
+                ssbk::dense_window_kernel<<<grid, 128, 0, stream>>>(G, out, stride, wLo, first);
+            });
+        }
+    }
 };
 
-int DeviceEngine::Impl::choose_block(int n, bool sparseInline) const {
+int DeviceEngine::Impl::choose_block(int n, const std::function<std::int64_t(int)>& smemFor,
+                                     const void* kernelFn) const {
     const int single = std::min(1024, round_up(std::max(n, 1), 32));
     if (cfg.blockSize > 0) return std::min(round_up(cfg.blockSize, 32), 1024);
+    if (n <= 256) return single;  // one block; extra threads serve the parallel phases
     int regs = 32, shared = 0, maxThreads = 1024;
-    kernel_attributes("condlif_window", regs, shared, maxThreads);
-    synscale::DeviceSpec dev = synscale::device_preset("sm100");
-    auto smemFor = [&](int bs) {
-        return static_cast<std::int64_t>(shared) + (sparseInline ? bs * 4 : 0);
-    };
-    if (cfg.blockPolicy == 1) {
-        // the paper's model as is: highest occupancy, ties to the larger block
-        // (reference occupancy.cpp:79-101), capped by what one block needs
-        const auto [bs, r] = synscale::recommend_block_size(dev, regs, smemFor(1024));
-        (void)r;
-        return std::min<int>(static_cast<int>(bs), single);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kernelFn) == cudaSuccess) {
+        regs = fa.numRegs;
+        shared = static_cast<int>(fa.sharedSizeBytes);
+        maxThreads = fa.maxThreadsPerBlock;
+    } else {
+        cudaGetLastError();
     }
-    // Default: the same model, restricted to block sizes whose grid still
-    // covers every SM (the model is per-SM and blind to wave quantisation).
+    const synscale::DeviceSpec dev = synscale::device_preset("sm100");
+    auto smem = [&](int bs) { return static_cast<std::int64_t>(shared) + smemFor(bs); };
+    auto fits = [&](int bs) { return smem(bs) <= 220 * 1024; };
     int best = 0;
     std::int64_t bestWarps = -1;
     for (int bs = 32; bs <= std::min(maxThreads, 1024); bs += 32) {
-        const int grid = (n + bs - 1) / bs;
-        if (grid < smCount && bs != 32) continue;
-        const auto r = synscale::occupancy(dev, {bs, regs, smemFor(bs)});
+        if (!fits(bs)) continue;
+        // default policy: the paper's model restricted to block sizes whose
+        // grid still covers every SM (the model is per-SM and blind to wave
+        // quantisation); policy 1: the model as is (reference
+        // occupancy.cpp:79-101: highest occupancy, ties to the larger block)
+        if (cfg.blockPolicy != 1 && (n + bs - 1) / bs < smCount && bs != 32) continue;
+        const auto r = synscale::occupancy(dev, {bs, regs, smem(bs)});
         if (r.activeWarps >= bestWarps) {
             bestWarps = r.activeWarps;
             best = bs;
         }
     }
-    if (best == 0 || (n + best - 1) / best < smCount) return single;  // small population
-    return best;
+    if (best == 0) best = 32;
+    return std::min(best, single);
+}
+
+// Shared-memory layout of a CondLif population kernel for tiles of tileN
+// neurons (StageGroup in kernels.cuh): staging regions, the phase-A input
+// buffer s_in [2][C][tileN] and, for single-block populations, a copy of the
+// window's spike bits.  Dense weight tiles are dropped from the plan (read
+// from L2 instead) when the whole plan would not fit.  Returns the bytes.
+int DeviceEngine::Impl::plan_stage(const HostNet& net, int pi, int tileN, ssbk::StageAcc out[2],
+                                   int& offIn, int& C, int& offBits) const {
+    const auto& P = pops[pi];
+    auto align = [](std::int64_t v, std::int64_t a) { return (v + a - 1) / a * a; };
+    const int W = Wmax;
+    const bool single = P.n <= tileN;
+    std::int64_t total = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        const bool allowW = pass == 0;
+        std::int64_t off = 0;
+        for (int a = 0; a < 2; ++a) {
+            out[a] = ssbk::StageAcc{};
+            const auto& A = P.acc[a];
+            if (A.mode != ssbk::kAccInline) continue;
+            for (int k = 0; k < A.ng; ++k) {
+                const auto& g = net.groups[P.accGroups[a][k]];
+                const int preN = net.pops[g.pre].n;
+                auto& S = out[a].g[k];
+                S.listCap = static_cast<int>(
+                    std::min<std::int64_t>(static_cast<std::int64_t>(W) * preN, 2048));
+                S.offCnt = static_cast<int>(off);
+                off += (W + 1) * 4;
+                S.offList = static_cast<int>(off);
+                off += static_cast<std::int64_t>(S.listCap) * 4;
+                if (g.dense) {
+                    const std::int64_t wbytes = static_cast<std::int64_t>(g.preCount) * tileN * 4;
+                    if (allowW && wbytes <= 96 * 1024) {
+                        S.stageW = 1;
+                        off = align(off, 16);
+                        S.offW = static_cast<int>(off);
+                        off += wbytes;
+                    }
+                } else {
+                    S.offLo = static_cast<int>(off);
+                    off += static_cast<std::int64_t>(S.listCap) * 4;
+                    S.offEoff = static_cast<int>(off);
+                    off += static_cast<std::int64_t>(S.listCap + 1) * 4;
+                    const double perRow = g.preCount > 0 ? static_cast<double>(g.nnz) /
+                                                               g.preCount * tileN /
+                                                               std::max(1, g.nPost)
+                                                         : 0.0;
+                    S.entCap = static_cast<int>(std::min<double>(
+                        4096.0, std::max(512.0, S.listCap * (1.5 * perRow + 4.0))));
+                    S.offEidx = static_cast<int>(off);
+                    off += static_cast<std::int64_t>(S.entCap) * 2;
+                    off = align(off, 4);
+                    S.offEg = static_cast<int>(off);
+                    off += static_cast<std::int64_t>(S.entCap) * 4;
+                }
+            }
+        }
+        const std::int64_t inBudget =
+            std::max<std::int64_t>(16 * 1024, std::min<std::int64_t>(single ? 96 * 1024 : 64 * 1024,
+                                                                     200 * 1024 - off));
+        C = static_cast<int>(std::clamp<std::int64_t>(inBudget / (2LL * tileN * 4), 4, 64));
+        C = std::min(C, W);
+        off = align(off, 16);
+        offIn = static_cast<int>(off);
+        off += 2LL * C * tileN * 4;
+        offBits = -1;
+        if (single && P.nwords <= 32) {
+            offBits = static_cast<int>(off);
+            off += static_cast<std::int64_t>(W) * P.nwords * 4;
+        }
+        total = align(off, 16);
+        if (total <= 200 * 1024) break;
+    }
+    return static_cast<int>(total);
 }
 
 void DeviceEngine::Impl::build(const HostNet& net) {
@@ -296,8 +431,23 @@ void DeviceEngine::Impl::build(const HostNet& net) {
                     if (!net.groups[gi].dense) P.sparseInline = true;
         }
         if (hp.kind == kCondLif) {
-            P.block = choose_block(hp.n, P.sparseInline);
-            P.grid = (hp.n + P.block - 1) / P.block;
+            // tile size from the occupancy model (registers of the kernel +
+            // this tile's shared-memory plan, 1 KB per-block reservation)
+            ssbk::StageAcc tmp[2];
+            int tmpIn, tmpC, tmpBits;
+            P.tileN = choose_block(
+                hp.n,
+                [&](int tn) {
+                    return plan_stage(net, pi, tn, tmp, tmpIn, tmpC, tmpBits) + 1024;
+                },
+                reinterpret_cast<const void*>(&ssbk::condlif_window_kernel));
+            P.grid = (hp.n + P.tileN - 1) / P.tileN;
+            // a single-block population gets extra threads for the parallel phases
+            P.block = P.grid == 1 ? P.tileN * std::max(1, 256 / P.tileN) : P.tileN;
+            P.smemBytes = plan_stage(net, pi, P.tileN, P.stage, P.offIn, P.chunk, P.offBits);
+            if (P.smemBytes > 220 * 1024)
+                throw synscale::SpecError("population '" + hp.name +
+                                          "': shared-memory staging plan exceeds the SM budget");
         } else {
             P.block = 320;
             P.grid = 1;
@@ -364,7 +514,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         if (g.dense) {
             G.W = upload<float>(g.W, static_cast<std::size_t>(g.nPre) * g.nPost);
         } else {
-            G.segTile = post.kind == kCondLif ? post.block : 256;
+            G.segTile = post.kind == kCondLif ? post.tileN : 256;
             G.nTiles = (g.nPost + G.segTile - 1) / G.segTile;
             G.g = upload<float>(g.g, static_cast<std::size_t>(g.nnz));
             G.ind = upload<int>(g.ind, static_cast<std::size_t>(g.nnz));
@@ -401,9 +551,12 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         raster.list[pi] = pops[pi].dev.list;
     }
     const std::int64_t perWindow = static_cast<std::int64_t>(Wmax) * totalNeurons;
-    rasterCap = cfg.rasterCapacity > 0 ? cfg.rasterCapacity
-                                       : std::max<std::int64_t>(std::int64_t(1) << 24, 2 * perWindow);
-    rasterCap = std::max(rasterCap, perWindow);
+    rasterCap = cfg.rasterCapacity > 0
+                    ? cfg.rasterCapacity
+                    : std::max<std::int64_t>(std::int64_t(1) << 26, (kRing + 2) * perWindow);
+    rasterCap = std::max(rasterCap, (kRing + 1) * perWindow);
+    CK(cudaMallocHost(&ringVal, kRing * sizeof(long long)));
+    for (auto& e : ringEv) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     raster.arena = alloc<int>(static_cast<std::size_t>(rasterCap));
     raster.cursor = alloc<long long>(2);
     raster.countsAll = alloc<int>(static_cast<std::size_t>(std::max<std::int64_t>(stepsTotal, 1)) *
@@ -413,8 +566,15 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     raster.doneCounter = alloc<unsigned>(1);
 
     // kernels with large dynamic shared tiles
+    int maxSmem = 0;
+    for (const auto& P : pops) maxSmem = std::max(maxSmem, P.smemBytes);
     CK(cudaFuncSetAttribute(ssbk::condlif_window_kernel,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 4));
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(maxSmem, 4096)));
+    CK(cudaFuncSetAttribute(ssbk::dense_window_tma_kernel,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, ring_smem(kRowBlock, true)));
+    CK(cudaFuncSetAttribute(ssbk::dense_window_pipe_kernel,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, ring_smem(kRowBlock, false)));
+    if (const char* e = std::getenv("SSB_DENSE_KERNEL")) useTma = std::string(e) == "tma";
     CK(cudaFuncSetAttribute(ssbk::sparse_window_kernel,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 4));
     CK(cudaStreamSynchronize(stream));
@@ -425,8 +585,10 @@ void DeviceEngine::Impl::enqueue_window(int W) {
         auto& P = pops[pi];
         if (P.kind == kPoisson) {
             launch("poisson_window:" + P.name, [&] {
-                ssbk::poisson_window_kernel<<<1, 320, 0, stream>>>(P.dev, W, P.acc[0].mode,
-                                                                   P.acc[1].mode);
+                const int bitsBytes = W * P.nwords * 4;
+                const int inSmem = bitsBytes <= 32 * 1024;
+                ssbk::poisson_window_kernel<<<1, 320, inSmem ? bitsBytes : 0, stream>>>(
+                    P.dev, W, P.acc[0].mode, P.acc[1].mode, inSmem);
             });
             continue;
         }
@@ -437,11 +599,7 @@ void DeviceEngine::Impl::enqueue_window(int W) {
                 const int gi = P.accGroups[a][k];
                 float* out = P.acc[a].buf + P.n;  // row w = 1
                 if (G.dense) {
-                    dim3 grid((G.nPost + 127) / 128, W);
-                    launch("dense_window:" + groupMeta[gi].name, [&] {
-                        ssbk::dense_window_kernel<<<grid, 128, 0, stream>>>(G, out, P.n, 1,
-                                                                            k == 0);
-                    });
+                    launch_dense(G, groupMeta[gi].name, "dense_window:", out, P.n, 1, W, k == 0);
                 } else {
                     dim3 grid(G.nTiles, W);
                     launch("sparse_window:" + groupMeta[gi].name, [&] {
@@ -451,10 +609,10 @@ void DeviceEngine::Impl::enqueue_window(int W) {
                 }
             }
         }
-        const int smem = P.sparseInline ? P.block * 4 : 0;
         launch("condlif_window:" + P.name, [&] {
-            ssbk::condlif_window_kernel<<<P.grid, P.block, smem, stream>>>(P.dev, P.acc[0],
-                                                                         P.acc[1], W);
+            ssbk::condlif_window_kernel<<<P.grid, P.block, P.smemBytes, stream>>>(
+                P.dev, P.acc[0], P.acc[1], P.stage[0], P.stage[1], W, P.tileN, P.chunk, P.offIn,
+                P.offBits);
         });
         if (P.grid > 1) {
             const int bs = std::min(1024, round_up(P.nwords, 32));
@@ -474,10 +632,7 @@ void DeviceEngine::Impl::enqueue_window(int W) {
                 const auto& G = P.acc[a].g[k];
                 const int gi = P.accGroups[a][k];
                 if (G.dense) {
-                    dim3 grid((G.nPost + 127) / 128, 1);
-                    launch("dense_deliver:" + groupMeta[gi].name, [&] {
-                        ssbk::dense_window_kernel<<<grid, 128, 0, stream>>>(G, out, 0, W, k == 0);
-                    });
+                    launch_dense(G, groupMeta[gi].name, "dense_deliver:", out, 0, W, 1, k == 0);
                 } else {
                     dim3 grid(G.nTiles, 1);
                     launch("sparse_deliver:" + groupMeta[gi].name, [&] {
@@ -507,19 +662,30 @@ void DeviceEngine::Impl::flush_raster() {
     }
     const long long zero = 0;
     CK(cudaMemcpy(raster.cursor + parity, &zero, sizeof(long long), cudaMemcpyHostToDevice));
-    eventBound = 0;
+    knownCursor = 0;
+    knownWin = epochStart = windowsLaunched;
 }
 
 void DeviceEngine::Impl::run_window(int W) {
     const std::int64_t add = static_cast<std::int64_t>(W) * totalNeurons;
-    if (eventBound + add > rasterCap) flush_raster();
-    eventBound += add;
+    // learn the cursor of the window kRing back (bounds the host's run-ahead)
+    if (windowsLaunched - kRing >= std::max(epochStart, knownWin)) {
+        const std::int64_t idx = windowsLaunched - kRing;
+        CK(cudaEventSynchronize(ringEv[idx % kRing]));
+        knownCursor = ringVal[idx % kRing];
+        knownWin = idx + 1;
+    }
+    std::int64_t bound = knownCursor + add;
+    for (std::int64_t w = knownWin; w < windowsLaunched; ++w) bound += ringAdd[w % kRing];
+    if (bound > rasterCap) flush_raster();
     if (cfg.useGraphs && !cfg.profile) {
         auto it = graphs.find(W);
         if (it == graphs.end()) {
             cudaGraph_t g;
             CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+            enqueued = 0;
             enqueue_window(W);
+            kernelsPerWindow[W] = enqueued;
             CK(cudaStreamEndCapture(stream, &g));
             cudaGraphExec_t exec;
             CK(cudaGraphInstantiate(&exec, g, 0));
@@ -527,10 +693,18 @@ void DeviceEngine::Impl::run_window(int W) {
             it = graphs.emplace(W, exec).first;
         }
         CK(cudaGraphLaunch(it->second, stream));
+        kernelLaunches += kernelsPerWindow[W];
     } else {
+        enqueued = 0;
         enqueue_window(W);
+        kernelLaunches += enqueued;
         harvest();
     }
+    const int slot = static_cast<int>(windowsLaunched % kRing);
+    CK(cudaMemcpyAsync(ringVal + slot, raster.cursor + ((windowsLaunched + 1) & 1),
+                       sizeof(long long), cudaMemcpyDeviceToHost, stream));
+    CK(cudaEventRecord(ringEv[slot], stream));
+    ringAdd[slot] = add;
     ++windowsLaunched;
     stepsDone += W;
 }
@@ -566,6 +740,9 @@ DeviceEngine::~DeviceEngine() {
         cudaEventDestroy(ev.second);
     }
     for (cudaEvent_t e : m.eventPool) cudaEventDestroy(e);
+    for (cudaEvent_t e : m.ringEv)
+        if (e) cudaEventDestroy(e);
+    if (m.ringVal) cudaFreeHost(m.ringVal);
     for (void* p : m.allocations) cudaFree(p);
     if (m.stream) cudaStreamDestroy(m.stream);
 }
@@ -663,6 +840,7 @@ int DeviceEngine::window() const { return impl_->Wmax; }
 int DeviceEngine::block_size(int pop) const { return impl_->pops.at(pop).block; }
 bool DeviceEngine::step_mode() const { return impl_->stepMode; }
 std::int64_t DeviceEngine::device_bytes() const { return impl_->bytes; }
+std::int64_t DeviceEngine::kernel_launches() const { return impl_->kernelLaunches; }
 
 std::vector<KernelStat> DeviceEngine::kernel_stats() {
     auto& m = *impl_;

@@ -116,6 +116,7 @@ public:
     int block_size(int pop) const;
     bool step_mode() const;
     std::int64_t device_bytes() const;
+    std::int64_t kernel_launches() const;  // kernels launched by step() so far
     std::vector<KernelStat> kernel_stats();
     void reset_kernel_stats();
 

@@ -698,6 +698,10 @@ int ssb_kernel_stats_reset(ssb_sim* sim) {
 
 int64_t ssb_device_bytes(const ssb_sim* sim) { return sim ? sim->core->engine().device_bytes() : 0; }
 
+int64_t ssb_kernel_launches(const ssb_sim* sim) {
+    return sim ? sim->core->engine().kernel_launches() : 0;
+}
+
 int ssb_device_preset(const char* name, ssb_device_spec* out, char* err, size_t errlen) {
     return guarded(err, errlen, [&] { to_c(device_preset(str(name)), out); });
 }

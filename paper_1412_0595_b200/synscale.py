@@ -489,8 +489,9 @@ class Simulation:
         else:
             a = np.ascontiguousarray(values, np.float32)
             fid = _FIELDS[fieldname]
-        self._check(lib.ssb_push_state(self._h, pi, fid, a.ctypes.data, a.size if fid !=
-                                       L.FIELD_FLAGGED else 1) if a.size == n else L.SSB_ERR_SPEC)
+        if a.size != n:
+            raise SpecError(f"state field '{fieldname}' holds {n} values, {a.size} given")
+        self._check(lib.ssb_push_state(self._h, pi, fid, a.ctypes.data, n))
 
     def population_state(self, name: str) -> PopulationState:
         """Snapshot of the device state (push edits back with push_state)."""
@@ -580,6 +581,9 @@ class Simulation:
 
     def device_bytes(self) -> int:
         return int(lib.ssb_device_bytes(self._h))
+
+    def kernel_launches(self) -> int:
+        return int(lib.ssb_kernel_launches(self._h))
 
 
 def run(spec: NetworkSpec, mode: StorageMode = StorageMode.FromSpec,

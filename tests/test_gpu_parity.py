@@ -212,7 +212,7 @@ def test_lifecycle_and_step_counts():
     with pytest.raises(S.SpecError):
         S.run(bad)
     over = specs.mbody_spec(100, 0.5, 1.0)
-    over.synapses[0].gScale = 1e39
+    over.synapses[0].gScale = 1e41  # U(0, 0.02) * 1e41 overflows fp32
     with pytest.raises(S.SpecError, match="overflow"):
         S.Simulation(over)
 
