@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -85,8 +86,12 @@ struct DeviceEngine::Impl {
         int kind = 0, n = 0, nwords = 0;
         int block = 0, grid = 0;
         bool sparseInline = false;  // needs a dynamic shared tile
-        ssbk::PopDev dev{};
-        ssbk::AccDev acc[2]{};
+        ssbk::PopDev dev{};             // state + window buffer set 0
+        ssbk::AccDev acc[2]{};          // accumulator plans (buffer set 0 views)
+        ssbk::PopDev devb[2]{};         // per window-buffer set b
+        ssbk::AccDev accb[2][2]{};      // [b][sign]
+        std::vector<int> prePops;       // populations whose spikes of the same window feed it
+        std::vector<int> consumers;     // populations reading its spike lists
         ssbk::StageAcc stage[2]{};  // shared-memory staging plan (condlif)
         int smemBytes = 0;          // dynamic shared memory of the population kernel
         int offBits = -1;           // shared copy of the window's spike bits (1-block pops)
@@ -208,9 +213,45 @@ struct DeviceEngine::Impl {
     int plan_stage(const HostNet& net, int pi, int tileN, ssbk::StageAcc out[2], int& offIn,
                    int& C, int& offBits) const;
     void build(const HostNet& net);
-    void enqueue_window(int W);
-    void run_window(int W);
+    void enqueue_pop(int pi, int W, int b, cudaStream_t s);
+    void enqueue_tail(int W, int b, cudaStream_t s);
+    void enqueue_windows(int W, int M);
+    void run_windows(int W, int M);
     void flush_raster();
+    void release();
+
+    // multi-window graphs
+    ssbk::RasterDev rasterb[2]{};
+    std::vector<cudaStream_t> auxStreams;
+    std::vector<cudaEvent_t> capEvents;
+    std::size_t evUsed = 0;
+    int graphWindows = 1;
+    // Wide kernels (a grid that fills a large part of the GPU with shared-
+    // memory-heavy blocks: KC's update, kc_dn's gather) are chained across
+    // streams so they never compete for SMs; narrow ones overlap them freely.
+    bool multiStream = false;
+    cudaEvent_t lastWide = nullptr;
+    bool is_wide(long long blocks, int smem) const {
+        return blocks >= smCount / 4 && smem >= 32 * 1024;
+    }
+    void before_wide(cudaStream_t s) {
+        if (multiStream && lastWide) CK(cudaStreamWaitEvent(s, lastWide, 0));
+    }
+    void after_wide(cudaStream_t s) {
+        if (!multiStream) return;
+        lastWide = capture_event();
+        CK(cudaEventRecord(lastWide, s));
+    }
+    std::int64_t launchesDone = 0;
+    std::map<int, int> kernelsPerLaunch;
+    cudaEvent_t capture_event() {
+        if (evUsed == capEvents.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            capEvents.push_back(e);
+        }
+        return capEvents[evUsed++];
+    }
 
     static constexpr int kRowBlock = 128;
     static int ring_smem(int bd, bool tma) {
@@ -223,23 +264,27 @@ struct DeviceEngine::Impl {
     // coalesced gathers otherwise.
     bool useTma = false;
     void launch_dense(const ssbk::GroupDev& G, const std::string& gname, const char* tag,
-                      float* out, long long stride, int wLo, int nW, int first) {
+                      float* out, long long stride, int wLo, int nW, int first, cudaStream_t s) {
         if (G.nPost % 4 == 0 && !useTma) {
             dim3 grid((G.nPost + kRowBlock - 1) / kRowBlock, nW);
+            const bool wide = is_wide(static_cast<long long>(grid.x) * grid.y,
+                                      ring_smem(kRowBlock, false));
+            if (wide) before_wide(s);
             launch(std::string(tag) + gname, [&] {
-                ssbk::dense_window_pipe_kernel<<<grid, kRowBlock, ring_smem(kRowBlock, false),
-                                                 stream>>>(G, out, stride, wLo, first);
+                ssbk::dense_window_pipe_kernel<<<grid, kRowBlock, ring_smem(kRowBlock, false), s>>>(
+                    G, out, stride, wLo, first);
             });
+            if (wide) after_wide(s);
         } else if (G.nPost % 4 == 0) {
             dim3 grid((G.nPost + kRowBlock - 1) / kRowBlock, nW);
             launch(std::string(tag) + gname, [&] {
-                ssbk::dense_window_tma_kernel<<<grid, kRowBlock, ring_smem(kRowBlock, true),
-                                                stream>>>(G, out, stride, wLo, first);
+                ssbk::dense_window_tma_kernel<<<grid, kRowBlock, ring_smem(kRowBlock, true), s>>>(
+                    G, out, stride, wLo, first);
             });
         } else {
             dim3 grid((G.nPost + 127) / 128, nW);
             launch(std::string(tag) + gname, [&] {
-                ssbk::dense_window_kernel<<<grid, 128, 0, stream>>>(G, out, stride, wLo, first);
+                ssbk::dense_window_kernel<<<grid, 128, 0, s>>>(G, out, stride, wLo, first);
             });
         }
     }
@@ -263,16 +308,30 @@ int DeviceEngine::Impl::choose_block(int n, const std::function<std::int64_t(int
     auto smem = [&](int bs) { return static_cast<std::int64_t>(shared) + smemFor(bs); };
     auto fits = [&](int bs) { return smem(bs) <= 220 * 1024; };
     int best = 0;
-    std::int64_t bestWarps = -1;
+    std::int64_t bestWarps = -1, bestLoad = INT64_MAX;
     for (int bs = 32; bs <= std::min(maxThreads, 1024); bs += 32) {
         if (!fits(bs)) continue;
-        // default policy: the paper's model restricted to block sizes whose
-        // grid still covers every SM (the model is per-SM and blind to wave
-        // quantisation); policy 1: the model as is (reference
-        // occupancy.cpp:79-101: highest occupancy, ties to the larger block)
-        if (cfg.blockPolicy != 1 && (n + bs - 1) / bs < smCount && bs != 32) continue;
         const auto r = synscale::occupancy(dev, {bs, regs, smem(bs)});
-        if (r.activeWarps >= bestWarps) {
+        if (cfg.blockPolicy == 1) {
+            // the paper's model as is (reference occupancy.cpp:79-101):
+            // highest occupancy, ties to the larger block
+            if (r.activeWarps >= bestWarps) {
+                bestWarps = r.activeWarps;
+                best = bs;
+            }
+            continue;
+        }
+        // default: the model's resident blocks per SM, plus the wave
+        // quantisation it is blind to — minimise the neurons the busiest SM
+        // advances (waves x resident blocks x tile), ties to more warps
+        if (r.activeBlocks < 1) continue;
+        const std::int64_t grid = (n + bs - 1) / bs;
+        const std::int64_t perWave = static_cast<std::int64_t>(smCount) * r.activeBlocks;
+        const std::int64_t waves = (grid + perWave - 1) / perWave;
+        const std::int64_t resident = std::min<std::int64_t>(r.activeBlocks, (grid + smCount - 1) / smCount);
+        const std::int64_t load = waves * resident * bs;
+        if (load < bestLoad || (load == bestLoad && r.activeWarps >= bestWarps)) {
+            bestLoad = load;
             bestWarps = r.activeWarps;
             best = bs;
         }
@@ -484,6 +543,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         d.synDecay = hp.synDecay;
         d.dt = net.dtS;
         d.p = hp.p;
+        // k * 2^-53 < p  <=>  k < p * 2^53 (exact scaling)  <=>  k < ceil(p * 2^53)
+        d.pThresh = static_cast<unsigned long long>(std::ceil(std::ldexp(hp.p, 53)));
         d.mt = upload<unsigned long long>(reinterpret_cast<const unsigned long long*>(hp.mt.data()),
                                           312);
         d.mtPos = upload<int>(&hp.mtPos, 1);
@@ -495,6 +556,28 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         for (int a = 0; a < 2; ++a)
             if (P.acc[a].mode == ssbk::kAccBuffered)
                 P.acc[a].buf = alloc<float>(static_cast<std::size_t>(Wmax + 1) * n);
+        // second window-buffer set: windows m and m+1 of one graph are in flight
+        // at once (spike lists, bitmasks, counts, buffered inputs)
+        P.devb[0] = d;
+        P.devb[1] = d;
+        P.devb[1].bits = alloc<uint32_t>(static_cast<std::size_t>(Wmax) * P.nwords);
+        P.devb[1].list = alloc<int>(static_cast<std::size_t>(Wmax) * n);
+        P.devb[1].count = alloc<int>(static_cast<std::size_t>(Wmax));
+        for (int a = 0; a < 2; ++a) {
+            P.accb[0][a] = P.acc[a];
+            P.accb[1][a] = P.acc[a];
+            if (P.acc[a].mode == ssbk::kAccBuffered)
+                P.accb[1][a].buf = alloc<float>(static_cast<std::size_t>(Wmax + 1) * n);
+        }
+    }
+    for (const auto& g : net.groups) {
+        if (stepMode || net.pops[g.post].kind == kPoisson) continue;  // inputs via state
+        auto& pp = pops[g.post].prePops;
+        if (std::find(pp.begin(), pp.end(), g.pre) == pp.end()) pp.push_back(g.pre);
+    }
+    for (const auto& g : net.groups) {
+        auto& c = pops[g.pre].consumers;
+        if (std::find(c.begin(), c.end(), g.post) == c.end()) c.push_back(g.post);
     }
 
     // groups
@@ -541,7 +624,16 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     }
     for (auto& P : pops)
         for (int a = 0; a < 2; ++a)
-            for (int k = 0; k < P.acc[a].ng; ++k) P.acc[a].g[k] = groupDev[P.accGroups[a][k]];
+            for (int k = 0; k < P.acc[a].ng; ++k) {
+                const int gi = P.accGroups[a][k];
+                P.acc[a].g[k] = groupDev[gi];
+                for (int b = 0; b < 2; ++b) {
+                    ssbk::GroupDev G = groupDev[gi];
+                    G.preList = pops[net.groups[gi].pre].devb[b].list;
+                    G.preCnt = pops[net.groups[gi].pre].devb[b].count;
+                    P.accb[b][a].g[k] = G;
+                }
+            }
 
     // raster arena
     raster.nPops = nPops;
@@ -550,11 +642,21 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         raster.count[pi] = pops[pi].dev.count;
         raster.list[pi] = pops[pi].dev.list;
     }
+    // windows per graph launch (overlap across windows needs an acyclic graph)
+    graphWindows = stepMode ? 1 : 4;
+    if (const char* e = std::getenv("SSB_GRAPH_WINDOWS"))
+        if (!stepMode) graphWindows = std::max(1, std::atoi(e));
+    // The host runs at most kRing launches ahead of the last cursor it has
+    // seen, so the arena must hold kRing + 1 launches of worst-case events
+    // (every neuron spiking every step); beyond ~2G events shrink the launch.
     const std::int64_t perWindow = static_cast<std::int64_t>(Wmax) * totalNeurons;
+    while (graphWindows > 1 && (kRing + 1) * perWindow * graphWindows > (std::int64_t(1) << 31))
+        graphWindows /= 2;
+    const std::int64_t perLaunch = perWindow * graphWindows;
     rasterCap = cfg.rasterCapacity > 0
                     ? cfg.rasterCapacity
-                    : std::max<std::int64_t>(std::int64_t(1) << 26, (kRing + 2) * perWindow);
-    rasterCap = std::max(rasterCap, (kRing + 1) * perWindow);
+                    : std::max<std::int64_t>(std::int64_t(1) << 26, (kRing + 1) * perLaunch);
+    rasterCap = std::max(rasterCap, (kRing + 1) * perLaunch);
     CK(cudaMallocHost(&ringVal, kRing * sizeof(long long)));
     for (auto& e : ringEv) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     raster.arena = alloc<int>(static_cast<std::size_t>(rasterCap));
@@ -564,6 +666,16 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     raster.stepCounter = alloc<long long>(1);
     raster.windowCounter = alloc<long long>(1);
     raster.doneCounter = alloc<unsigned>(1);
+    for (int b = 0; b < 2; ++b) {
+        rasterb[b] = raster;
+        for (int pi = 0; pi < nPops; ++pi) {
+            rasterb[b].count[pi] = pops[pi].devb[b].count;
+            rasterb[b].list[pi] = pops[pi].devb[b].list;
+        }
+    }
+    // capture streams: one per population, one for deliver + raster
+    auxStreams.resize(nPops + 1);
+    for (auto& s : auxStreams) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
 
     // kernels with large dynamic shared tiles
     int maxSmem = 0;
@@ -580,73 +692,135 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     CK(cudaStreamSynchronize(stream));
 }
 
-void DeviceEngine::Impl::enqueue_window(int W) {
-    for (int pi : order) {
-        auto& P = pops[pi];
-        if (P.kind == kPoisson) {
-            launch("poisson_window:" + P.name, [&] {
-                const int bitsBytes = W * P.nwords * 4;
-                const int inSmem = bitsBytes <= 32 * 1024;
-                ssbk::poisson_window_kernel<<<1, 320, inSmem ? bitsBytes : 0, stream>>>(
-                    P.dev, W, P.acc[0].mode, P.acc[1].mode, inSmem);
-            });
-            continue;
-        }
-        for (int a = 0; a < 2; ++a) {
-            if (P.acc[a].mode != ssbk::kAccBuffered) continue;
-            for (int k = 0; k < P.acc[a].ng; ++k) {
-                const auto& G = P.acc[a].g[k];
-                const int gi = P.accGroups[a][k];
-                float* out = P.acc[a].buf + P.n;  // row w = 1
-                if (G.dense) {
-                    launch_dense(G, groupMeta[gi].name, "dense_window:", out, P.n, 1, W, k == 0);
-                } else {
-                    dim3 grid(G.nTiles, W);
-                    launch("sparse_window:" + groupMeta[gi].name, [&] {
-                        ssbk::sparse_window_kernel<<<grid, G.segTile, G.segTile * 4, stream>>>(
-                            G, out, P.n, 1, k == 0);
-                    });
-                }
+// One population's kernels for one window on stream s, window-buffer set b.
+void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t s) {
+    auto& P = pops[pi];
+    const ssbk::PopDev& D = P.devb[b];
+    if (P.kind == kPoisson) {
+        launch("poisson_window:" + P.name, [&] {
+            const int bitsBytes = W * P.nwords * 4;
+            const int inSmem = bitsBytes <= 32 * 1024;
+            ssbk::poisson_window_kernel<<<1, 320, inSmem ? bitsBytes : 0, s>>>(
+                D, W, P.acc[0].mode, P.acc[1].mode, inSmem);
+        });
+        return;
+    }
+    for (int a = 0; a < 2; ++a) {
+        const auto& A = P.accb[b][a];
+        if (A.mode != ssbk::kAccBuffered) continue;
+        for (int k = 0; k < A.ng; ++k) {
+            const auto& G = A.g[k];
+            const int gi = P.accGroups[a][k];
+            float* out = A.buf + P.n;  // row w = 1
+            if (G.dense) {
+                launch_dense(G, groupMeta[gi].name, "dense_window:", out, P.n, 1, W, k == 0, s);
+            } else {
+                dim3 grid(G.nTiles, W);
+                launch("sparse_window:" + groupMeta[gi].name, [&] {
+                    ssbk::sparse_window_kernel<<<grid, G.segTile, G.segTile * 4, s>>>(G, out, P.n, 1,
+                                                                                     k == 0);
+                });
             }
         }
-        launch("condlif_window:" + P.name, [&] {
-            ssbk::condlif_window_kernel<<<P.grid, P.block, P.smemBytes, stream>>>(
-                P.dev, P.acc[0], P.acc[1], P.stage[0], P.stage[1], W, P.tileN, P.chunk, P.offIn,
-                P.offBits);
-        });
-        if (P.grid > 1) {
-            const int bs = std::min(1024, round_up(P.nwords, 32));
-            launch("compact_window:" + P.name, [&] {
-                ssbk::compact_window_kernel<<<W, bs, 0, stream>>>(P.dev.bits, P.nwords, P.n,
-                                                                  P.dev.list, P.dev.count);
-            });
-        }
     }
-    // accumulators written after every population advanced (cyclic graphs,
-    // Poisson targets): inputs of the next step from the last step's spikes
+    const bool wide = is_wide(P.grid, P.smemBytes);
+    if (wide) before_wide(s);
+    launch("condlif_window:" + P.name, [&] {
+        ssbk::condlif_window_kernel<<<P.grid, P.block, P.smemBytes, s>>>(
+            D, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk, P.offIn,
+            P.offBits);
+    });
+    if (P.grid > 1) {
+        const int bs = std::min(1024, round_up(P.nwords, 32));
+        launch("compact_window:" + P.name, [&] {
+            ssbk::compact_window_kernel<<<W, bs, 0, s>>>(D.bits, P.nwords, P.n, D.list, D.count);
+        });
+    }
+    if (wide) after_wide(s);
+}
+
+// Accumulators written after every population advanced (cyclic graphs,
+// Poisson targets: inputs of the next step from the last step's spikes), then
+// the window's raster.
+void DeviceEngine::Impl::enqueue_tail(int W, int b, cudaStream_t s) {
     for (auto& P : pops) {
         for (int a = 0; a < 2; ++a) {
-            if (P.acc[a].mode != ssbk::kAccDeliver) continue;
+            const auto& A = P.accb[b][a];
+            if (A.mode != ssbk::kAccDeliver) continue;
             float* out = a == 0 ? P.dev.excIn : P.dev.inhIn;
-            for (int k = 0; k < P.acc[a].ng; ++k) {
-                const auto& G = P.acc[a].g[k];
+            for (int k = 0; k < A.ng; ++k) {
+                const auto& G = A.g[k];
                 const int gi = P.accGroups[a][k];
                 if (G.dense) {
-                    launch_dense(G, groupMeta[gi].name, "dense_deliver:", out, 0, W, 1, k == 0);
+                    launch_dense(G, groupMeta[gi].name, "dense_deliver:", out, 0, W, 1, k == 0, s);
                 } else {
                     dim3 grid(G.nTiles, 1);
                     launch("sparse_deliver:" + groupMeta[gi].name, [&] {
-                        ssbk::sparse_window_kernel<<<grid, G.segTile, G.segTile * 4, stream>>>(
-                            G, out, 0, W, k == 0);
+                        ssbk::sparse_window_kernel<<<grid, G.segTile, G.segTile * 4, s>>>(G, out, 0,
+                                                                                         W, k == 0);
                     });
                 }
             }
         }
     }
-    const int rb = 128;
     launch("raster_window", [&] {
-        ssbk::raster_window_kernel<<<W * raster.nPops, rb, 0, stream>>>(raster, W);
+        ssbk::raster_window_kernel<<<W * raster.nPops, 128, 0, s>>>(rasterb[b], W);
     });
+}
+
+// M consecutive windows.  Each population's kernels run on its own stream;
+// cross-stream edges carry exactly the data dependencies: the pre
+// populations' spike lists of the same window, the reuse of a window-buffer
+// set two windows later (all readers done), deliver-before-next-window in
+// step mode, and raster order.  So PN / LHI of window m+1 overlap KC of
+// window m, and kc_dn / DN of window m overlap KC of window m+1.
+void DeviceEngine::Impl::enqueue_windows(int W, int M) {
+    const int nPops = static_cast<int>(pops.size());
+    const bool multi = !cfg.profile;  // profile mode: one stream, serial order
+    const int rs = nPops;
+    auto S = [&](int idx) { return multi ? auxStreams[idx] : stream; };
+    evUsed = 0;
+    multiStream = multi;
+    lastWide = nullptr;
+    auto mark = [&](int sidx) -> cudaEvent_t {
+        if (!multi) return nullptr;
+        cudaEvent_t e = capture_event();
+        CK(cudaEventRecord(e, S(sidx)));
+        return e;
+    };
+    auto after = [&](int sidx, cudaEvent_t e) {
+        if (multi && e) CK(cudaStreamWaitEvent(S(sidx), e, 0));
+    };
+    if (multi) {
+        cudaEvent_t fork = capture_event();
+        CK(cudaEventRecord(fork, stream));
+        for (auto s : auxStreams) CK(cudaStreamWaitEvent(s, fork, 0));
+    }
+    std::vector<std::vector<cudaEvent_t>> kdone(nPops, std::vector<cudaEvent_t>(M, nullptr));
+    std::vector<cudaEvent_t> rdone(M, nullptr);
+    for (int m = 0; m < M; ++m) {
+        const int b = m & 1;
+        for (int pi : order) {
+            auto& P = pops[pi];
+            for (int q : P.prePops) after(pi, kdone[q][m]);
+            if (m >= 2) {  // buffer set b was last read by window m-2's consumers
+                for (int c : P.consumers) after(pi, kdone[c][m - 2]);
+                after(pi, rdone[m - 2]);
+            }
+            if (stepMode && m >= 1) after(pi, rdone[m - 1]);
+            enqueue_pop(pi, W, b, S(pi));
+            kdone[pi][m] = mark(pi);
+        }
+        for (int pi = 0; pi < nPops; ++pi) after(rs, kdone[pi][m]);
+        enqueue_tail(W, b, S(rs));
+        rdone[m] = mark(rs);
+    }
+    if (multi)
+        for (auto s : auxStreams) {
+            cudaEvent_t e = capture_event();
+            CK(cudaEventRecord(e, s));
+            CK(cudaStreamWaitEvent(stream, e, 0));
+        }
 }
 
 void DeviceEngine::Impl::flush_raster() {
@@ -663,50 +837,52 @@ void DeviceEngine::Impl::flush_raster() {
     const long long zero = 0;
     CK(cudaMemcpy(raster.cursor + parity, &zero, sizeof(long long), cudaMemcpyHostToDevice));
     knownCursor = 0;
-    knownWin = epochStart = windowsLaunched;
+    knownWin = epochStart = launchesDone;
 }
 
-void DeviceEngine::Impl::run_window(int W) {
-    const std::int64_t add = static_cast<std::int64_t>(W) * totalNeurons;
-    // learn the cursor of the window kRing back (bounds the host's run-ahead)
-    if (windowsLaunched - kRing >= std::max(epochStart, knownWin)) {
-        const std::int64_t idx = windowsLaunched - kRing;
+void DeviceEngine::Impl::run_windows(int W, int M) {
+    const std::int64_t add = static_cast<std::int64_t>(W) * M * totalNeurons;
+    // learn the cursor after the launch kRing back (bounds the host's run-ahead)
+    if (launchesDone - kRing >= std::max(epochStart, knownWin)) {
+        const std::int64_t idx = launchesDone - kRing;
         CK(cudaEventSynchronize(ringEv[idx % kRing]));
         knownCursor = ringVal[idx % kRing];
         knownWin = idx + 1;
     }
     std::int64_t bound = knownCursor + add;
-    for (std::int64_t w = knownWin; w < windowsLaunched; ++w) bound += ringAdd[w % kRing];
+    for (std::int64_t l = knownWin; l < launchesDone; ++l) bound += ringAdd[l % kRing];
     if (bound > rasterCap) flush_raster();
+    const int key = W * 64 + M;
     if (cfg.useGraphs && !cfg.profile) {
-        auto it = graphs.find(W);
+        auto it = graphs.find(key);
         if (it == graphs.end()) {
             cudaGraph_t g;
             CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
             enqueued = 0;
-            enqueue_window(W);
-            kernelsPerWindow[W] = enqueued;
+            enqueue_windows(W, M);
+            kernelsPerLaunch[key] = enqueued;
             CK(cudaStreamEndCapture(stream, &g));
             cudaGraphExec_t exec;
             CK(cudaGraphInstantiate(&exec, g, 0));
             CK(cudaGraphDestroy(g));
-            it = graphs.emplace(W, exec).first;
+            it = graphs.emplace(key, exec).first;
         }
         CK(cudaGraphLaunch(it->second, stream));
-        kernelLaunches += kernelsPerWindow[W];
+        kernelLaunches += kernelsPerLaunch[key];
     } else {
         enqueued = 0;
-        enqueue_window(W);
+        enqueue_windows(W, M);
         kernelLaunches += enqueued;
         harvest();
     }
-    const int slot = static_cast<int>(windowsLaunched % kRing);
-    CK(cudaMemcpyAsync(ringVal + slot, raster.cursor + ((windowsLaunched + 1) & 1),
-                       sizeof(long long), cudaMemcpyDeviceToHost, stream));
+    windowsLaunched += M;
+    stepsDone += static_cast<std::int64_t>(W) * M;
+    const int slot = static_cast<int>(launchesDone % kRing);
+    CK(cudaMemcpyAsync(ringVal + slot, raster.cursor + (windowsLaunched & 1), sizeof(long long),
+                       cudaMemcpyDeviceToHost, stream));
     CK(cudaEventRecord(ringEv[slot], stream));
     ringAdd[slot] = add;
-    ++windowsLaunched;
-    stepsDone += W;
+    ++launchesDone;
 }
 
 // ---------------------------------------------------------------------------
@@ -724,36 +900,52 @@ DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfg)
     try {
         m.build(net);
     } catch (...) {
-        for (void* p : m.allocations) cudaFree(p);
-        cudaStreamDestroy(m.stream);
+        m.release();
         throw;
     }
 }
 
-DeviceEngine::~DeviceEngine() {
-    auto& m = *impl_;
-    cudaSetDevice(m.cfg.device);
-    if (m.stream) cudaStreamSynchronize(m.stream);
-    for (auto& [w, g] : m.graphs) cudaGraphExecDestroy(g);
-    for (auto& [n, ev] : m.pending) {
+void DeviceEngine::Impl::release() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& [w, g] : graphs) cudaGraphExecDestroy(g);
+    graphs.clear();
+    for (auto& [n, ev] : pending) {
         cudaEventDestroy(ev.first);
         cudaEventDestroy(ev.second);
     }
-    for (cudaEvent_t e : m.eventPool) cudaEventDestroy(e);
-    for (cudaEvent_t e : m.ringEv)
-        if (e) cudaEventDestroy(e);
-    if (m.ringVal) cudaFreeHost(m.ringVal);
-    for (void* p : m.allocations) cudaFree(p);
-    if (m.stream) cudaStreamDestroy(m.stream);
+    pending.clear();
+    for (cudaEvent_t e : eventPool) cudaEventDestroy(e);
+    eventPool.clear();
+    for (cudaEvent_t e : capEvents) cudaEventDestroy(e);
+    capEvents.clear();
+    for (cudaEvent_t& e : ringEv)
+        if (e) cudaEventDestroy(e), e = nullptr;
+    if (ringVal) cudaFreeHost(ringVal), ringVal = nullptr;
+    for (void* p : allocations) cudaFree(p);
+    allocations.clear();
+    for (cudaStream_t s : auxStreams) cudaStreamDestroy(s);
+    auxStreams.clear();
+    if (stream) cudaStreamDestroy(stream), stream = nullptr;
+}
+
+DeviceEngine::~DeviceEngine() {
+    cudaSetDevice(impl_->cfg.device);
+    impl_->release();
 }
 
 void DeviceEngine::step(std::int64_t n) {
     auto& m = *impl_;
     CK(cudaSetDevice(m.cfg.device));
+    const std::int64_t full = static_cast<std::int64_t>(m.Wmax) * m.graphWindows;
     while (n > 0) {
-        const int W = static_cast<int>(std::min<std::int64_t>(m.Wmax, n));
-        m.run_window(W);
-        n -= W;
+        if (m.graphWindows > 1 && n >= full) {
+            m.run_windows(m.Wmax, m.graphWindows);
+            n -= full;
+        } else {
+            const int W = static_cast<int>(std::min<std::int64_t>(m.Wmax, n));
+            m.run_windows(W, 1);
+            n -= W;
+        }
     }
 }
 
