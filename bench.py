@@ -384,6 +384,7 @@ def main():
             "sim_wall": sim_seconds / t_max,
             "us_per_timestep": t_max / (sim_seconds * STEPS_PER_SIM_SECOND) * 1e6,
             "build_s": build_s,
+            "step_ms": [round(x * 1e3, 3) for x in times],
             "gpu_launches": int(launches), "clocks": clk, "roofline": roofline,
             "cpu_baseline": cpu, "e2e": e2e}
     print(json.dumps(line), flush=True)

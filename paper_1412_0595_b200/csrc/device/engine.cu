@@ -10,6 +10,7 @@
 #include <map>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../engine.hpp"
@@ -134,8 +135,20 @@ struct DeviceEngine::Impl {
     cudaEvent_t ringEv[kRing] = {};
     std::int64_t ringAdd[kRing] = {};
     std::int64_t knownCursor = 0, knownWin = 0, epochStart = 0;
-    std::vector<std::int32_t> hostNeurons;
     bool rasterDiscarded = false;
+    // Host copy of the raster: drained arenas, in order.  A flush switches the
+    // device to the other arena and drains the full one on a copy stream from
+    // a helper thread, so the simulation keeps running during the copy.
+    std::vector<std::pair<std::unique_ptr<std::int32_t[]>, std::size_t>> hostChunks;
+    int* arenaSelDev = nullptr;
+    int arenaSel = 0;
+    cudaStream_t copyStream = nullptr;
+    static constexpr std::size_t kPinnedInts = std::size_t(1) << 23;  // 32 MB per stage
+    std::int32_t* pinned[2] = {nullptr, nullptr};
+    std::thread copier;
+    void join_copier() {
+        if (copier.joinable()) copier.join();
+    }
 
     std::map<int, cudaGraphExec_t> graphs;
 
@@ -217,7 +230,7 @@ struct DeviceEngine::Impl {
     void enqueue_tail(int W, int b, cudaStream_t s);
     void enqueue_windows(int W, int M);
     void run_windows(int W, int M);
-    void flush_raster();
+    void flush_raster(bool wait = false);
     void release();
 
     // multi-window graphs
@@ -659,7 +672,12 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     rasterCap = std::max(rasterCap, (kRing + 1) * perLaunch);
     CK(cudaMallocHost(&ringVal, kRing * sizeof(long long)));
     for (auto& e : ringEv) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    raster.arena = alloc<int>(static_cast<std::size_t>(rasterCap));
+    raster.arena[0] = alloc<int>(static_cast<std::size_t>(rasterCap));
+    raster.arena[1] = alloc<int>(static_cast<std::size_t>(rasterCap));
+    arenaSelDev = alloc<int>(1);
+    raster.arenaSel = arenaSelDev;
+    CK(cudaStreamCreateWithFlags(&copyStream, cudaStreamNonBlocking));
+    for (auto& p : pinned) CK(cudaMallocHost(&p, kPinnedInts * 4));
     raster.cursor = alloc<long long>(2);
     raster.countsAll = alloc<int>(static_cast<std::size_t>(std::max<std::int64_t>(stepsTotal, 1)) *
                                   nPops);
@@ -823,16 +841,44 @@ void DeviceEngine::Impl::enqueue_windows(int W, int M) {
         }
 }
 
-void DeviceEngine::Impl::flush_raster() {
+// Switches the device to the other arena and drains the full one in the
+// background (wait = true: drain synchronously, e.g. to collect results).
+void DeviceEngine::Impl::flush_raster(bool wait) {
     CK(cudaStreamSynchronize(stream));
     long long cur = 0;
     const int parity = static_cast<int>(windowsLaunched & 1);
     CK(cudaMemcpy(&cur, raster.cursor + parity, sizeof(long long), cudaMemcpyDeviceToHost));
+    join_copier();  // the other arena must be drained before it is reused
+    const int full = arenaSel;
+    arenaSel ^= 1;
+    CK(cudaMemcpy(arenaSelDev, &arenaSel, sizeof(int), cudaMemcpyHostToDevice));
     if (cur > 0 && !rasterDiscarded) {
-        const std::size_t at = hostNeurons.size();
-        hostNeurons.resize(at + static_cast<std::size_t>(cur));
-        CK(cudaMemcpy(hostNeurons.data() + at, raster.arena, static_cast<std::size_t>(cur) * 4,
-                      cudaMemcpyDeviceToHost));
+        auto chunk = std::unique_ptr<std::int32_t[]>(new std::int32_t[static_cast<std::size_t>(cur)]);
+        std::int32_t* dst = chunk.get();
+        hostChunks.emplace_back(std::move(chunk), static_cast<std::size_t>(cur));
+        const int* src = raster.arena[full];
+        const int dev = cfg.device;
+        cudaStream_t cs = copyStream;
+        std::int32_t* stage[2] = {pinned[0], pinned[1]};
+        // pinned staging: async device->host pieces, host memcpy of the previous
+        // piece meanwhile (pageable destinations would serialise the driver)
+        auto drain = [dst, src, cur, dev, cs, stage] {
+            cudaSetDevice(dev);
+            const std::size_t total = static_cast<std::size_t>(cur), piece = kPinnedInts;
+            std::size_t prevOff = 0, prevLen = 0;
+            int k = 0;
+            for (std::size_t off = 0; off < total || prevLen; off += piece, k ^= 1) {
+                const std::size_t len = off < total ? std::min(piece, total - off) : 0;
+                if (len)
+                    cudaMemcpyAsync(stage[k], src + off, len * 4, cudaMemcpyDeviceToHost, cs);
+                if (prevLen) std::memcpy(dst + prevOff, stage[k ^ 1], prevLen * 4);
+                cudaStreamSynchronize(cs);
+                prevOff = off;
+                prevLen = len;
+            }
+        };
+        if (wait) drain();
+        else copier = std::thread(drain);
     }
     const long long zero = 0;
     CK(cudaMemcpy(raster.cursor + parity, &zero, sizeof(long long), cudaMemcpyHostToDevice));
@@ -906,6 +952,10 @@ DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfg)
 }
 
 void DeviceEngine::Impl::release() {
+    join_copier();
+    if (copyStream) cudaStreamDestroy(copyStream), copyStream = nullptr;
+    for (auto& p : pinned)
+        if (p) cudaFreeHost(p), p = nullptr;
     if (stream) cudaStreamSynchronize(stream);
     for (auto& [w, g] : graphs) cudaGraphExecDestroy(g);
     graphs.clear();
@@ -999,19 +1049,27 @@ void DeviceEngine::collect_raster(std::vector<std::int32_t>& counts,
     CK(cudaSetDevice(m.cfg.device));
     if (m.rasterDiscarded)
         throw synscale::SpecError("the raster was discarded (ssb_raster_discard)");
-    m.flush_raster();
+    m.flush_raster(true);
+    m.join_copier();
     const std::size_t nc = static_cast<std::size_t>(m.stepsDone) * m.pops.size();
     counts.resize(nc);
     if (nc)
         CK(cudaMemcpy(counts.data(), m.raster.countsAll, nc * 4, cudaMemcpyDeviceToHost));
-    neurons = m.hostNeurons;
+    std::size_t total = 0;
+    for (const auto& c : m.hostChunks) total += c.second;
+    neurons.resize(total);
+    std::size_t at = 0;
+    for (const auto& c : m.hostChunks) {
+        std::copy(c.first.get(), c.first.get() + c.second, neurons.data() + at);
+        at += c.second;
+    }
 }
 
 void DeviceEngine::discard_raster() {
     auto& m = *impl_;
-    m.flush_raster();
-    m.hostNeurons.clear();
-    m.hostNeurons.shrink_to_fit();
+    m.flush_raster(true);
+    m.join_copier();
+    m.hostChunks.clear();
     m.rasterDiscarded = true;
 }
 

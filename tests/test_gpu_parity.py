@@ -120,6 +120,22 @@ def test_chain_paths_match_oracle(oracle_mod, heavy, block):
     assert np.array_equal(rg.raster.neuron, ro[2]) and np.array_equal(rg.raster.step, ro[0])
 
 
+@pytest.mark.parametrize("graph_windows", ["1", "2", "4"])
+def test_raster_flushes_and_multiwindow_graphs(oracle_mod, monkeypatch, graph_windows):
+    """A minimal raster arena forces many background flushes (arena switches)
+    while multi-window graphs overlap populations; the raster must still be
+    the reference's, in order."""
+    monkeypatch.setenv("SSB_GRAPH_WINDOWS", graph_windows)
+    spec = specs.chain_spec(100.0)
+    g = gpu_sim(spec, window=9, rasterCapacity=1)
+    rg = g.finish()
+    o = cpu_sim(oracle_mod, spec)
+    ro = o.finish()
+    assert len(rg.raster) == len(ro[0]) > 100_000
+    assert np.array_equal(rg.raster.step, ro[0]) and np.array_equal(rg.raster.neuron, ro[2])
+    assert np.array_equal(rg.raster.population, ro[1])
+
+
 def test_fault_injection_spreads_like_reference(oracle_mod):
     """test_engine.cpp:402-434: a poisoned state written between steps."""
     spec = specs.mbody_spec(1000, 0.5, 5.0)
