@@ -89,20 +89,43 @@ class ClockSampler:
         self._t = None
 
     def start(self):
-        def run():
+        try:  # NVML: ~10 ms sampling, so even a short timed region gets many samples
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            bits = [(0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"),
+                    (0x20, "sw_thermal_slowdown"), (0x4, "sw_power_cap")]
+
+            def sample():
+                r = reasons(h)
+                return [str(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)), str(mx), "",
+                        ""] + ["Active" if r & b else "Not Active" for b, _ in bits]
+            sample()
+            period = 0.01
+        except Exception:
             q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+            def sample():
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                return [x.strip() for x in out.split(",")] if out else None
+            period = 0.2
+
+        def run():
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True,
-                                         text=True, timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
+                    v = sample()
+                    if v:
+                        self.samples.append(v)
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(period)
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
@@ -222,7 +245,7 @@ def run_reference_arm(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--window", type=int, default=256)
@@ -350,7 +373,9 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get(rf["kernel"].split(":")[0])
+            per = json.load(f).get("bytes_per_launch", {})
+        kname = rf["kernel"].split(":")[0]
+        traffic = per.get(kname, per.get(kname + "_kernel"))
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": rf["kernel"], "peak_source": peak_src,

@@ -1,0 +1,171 @@
+// test_facade.cpp — reference-style callers compiled against the drop-in
+// headers (include/synscale/*.hpp) and linked to libsynscale_b200.so.
+// Re-hosts, through the C++ API exactly as the reference's tests call it:
+//   test_engine.cpp:183-290  conductance neuron vs its reference integrator
+//   test_engine.cpp:124-181  one-step delivery latency (read via population_state)
+//   test_engine.cpp:292-333  propagate hand example and errors
+//   test_engine.cpp:402-434  fault injection through the mutable state reference
+//   test_engine.cpp:455-474  storage mode does not change results
+// Exit code 0 = all checks passed.  Needs a GPU (no CPU fallback).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <limits>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "synscale/engine.hpp"
+#include "synscale/io.hpp"
+#include "synscale/network.hpp"
+#include "synscale/random.hpp"
+
+using namespace synscale;
+
+static int failures = 0;
+#define CHECK(c)                                                        \
+    do {                                                                \
+        if (!(c)) {                                                     \
+            std::fprintf(stderr, "%s:%d CHECK failed: %s\n", __FILE__, __LINE__, #c); \
+            ++failures;                                                 \
+        }                                                               \
+    } while (0)
+
+template <typename F>
+static bool throws_spec(F&& f) {
+    try {
+        f();
+    } catch (const SpecError&) {
+        return true;
+    }
+    return false;
+}
+
+static void conductance_kat() {
+    NetworkSpec spec;
+    NeuronPopulation drive{"drive", 1, ModelKind::PoissonSource, 1, PoissonParams{200.0}};
+    NeuronPopulation damp{"damp", 1, ModelKind::PoissonSource, 2, PoissonParams{80.0}};
+    NeuronPopulation cell{"cell", 1, ModelKind::CondLif, 3, CondLifParams{}};
+    spec.populations = {drive, damp, cell};
+    SynapseGroupSpec exc;
+    exc.name = "exc";
+    exc.pre = "drive";
+    exc.post = "cell";
+    exc.outDegree = 1;
+    exc.baseWeight = WeightDist::constant(0.05);
+    SynapseGroupSpec inh = exc;
+    inh.name = "inh";
+    inh.pre = "damp";
+    inh.sign = SynapseSign::Inhibitory;
+    inh.baseWeight = WeightDist::constant(0.03);
+    spec.synapses = {exc, inh};
+    spec.dtMs = 1.0;
+    spec.durationMs = 400.0;
+    spec.globalSeed = 11;
+
+    Simulation sim(spec);
+    RandomStream excSrc(11, 1, "drive/source"), inhSrc(11, 2, "damp/source");
+    const CondLifParams lif;
+    const scalar dt = 1, tauM = scalar(lif.tauMMs), eLeak = scalar(lif.eLeakMV),
+                 eExc = scalar(lif.eExcMV), eInh = scalar(lif.eInhMV),
+                 vThresh = scalar(lif.vThreshMV), vReset = scalar(lif.vResetMV),
+                 synDecay = scalar(std::exp(-1.0 / lif.tauSynMs));
+    scalar v = eLeak, gExc = 0, gInh = 0, excIn = 0, inhIn = 0;
+    std::vector<std::int64_t> refSpikes;
+    for (std::int64_t t = 0; t < sim.steps_total(); ++t) {
+        sim.step();
+        const bool ef = excSrc.uniform01() < 0.2, hf = inhSrc.uniform01() < 0.08;
+        const scalar ge = gExc * synDecay + excIn;
+        const scalar gi = gInh * synDecay - inhIn;
+        v += dt * ((eLeak - v) / tauM + ge * (eExc - v) + gi * (eInh - v));
+        gExc = ge;
+        gInh = gi;
+        if (v >= vThresh) {
+            refSpikes.push_back(t);
+            v = vReset;
+        }
+        const auto& st = sim.population_state("cell");
+        CHECK(st.v[0] == v);
+        CHECK(st.gExc[0] == gExc);
+        CHECK(st.gInh[0] == gInh);
+        excIn = ef ? scalar(0.05) : scalar(0);
+        inhIn = hf ? scalar(-0.03) : scalar(0);
+        CHECK(sim.population_state("cell").excIn[0] == excIn);  // delivered one step later
+    }
+    RunResult r = sim.finish();
+    std::vector<std::int64_t> got;
+    for (const auto& e : r.raster.events)
+        if (e.population == 2) got.push_back(e.step);
+    CHECK(got == refSpikes);
+    CHECK(!refSpikes.empty());
+    CHECK(throws_spec([&] { sim.finish(); }));
+    CHECK(throws_spec([&] { sim.step(); }));
+}
+
+static void propagate_examples() {
+    DenseMatrix d;
+    d.nPre = 2;
+    d.nPost = 3;
+    d.weights = {0.f, 0.5f, 0.f, 0.2f, 0.f, 0.3f};
+    const CrsMatrix s = to_sparse(d);
+    std::vector<std::int32_t> spikes = {0, 1};
+    std::vector<scalar> a(3, 0.f), b(3, 0.f);
+    propagate(d, spikes, a);
+    propagate(s, spikes, b);
+    CHECK(a == (std::vector<scalar>{0.2f, 0.5f, 0.3f}));
+    CHECK(a == b);
+    std::vector<scalar> bad(2, 0.f);
+    CHECK(throws_spec([&] { propagate(d, spikes, bad); }));
+    std::vector<std::int32_t> oob = {2};
+    CHECK(throws_spec([&] { propagate(s, oob, a); }));
+}
+
+static void fault_injection_and_storage() {
+    std::map<std::string, double> gs = {{"pn_kc", 1e30}, {"pn_lhi", 1e30}, {"lhi_kc", 1e30},
+                                        {"kc_dn", 1e30}};
+    MBodyBuildOptions o;
+    o.dtMs = 0.1;
+    o.durationMs = 5.0;
+    NetworkSpec spec = build_mbody_net(100, 20, 1000, 100, gs, 7, o);
+    Simulation sim(spec);
+    // CondLif has no v*v term to overflow (the reference test uses Izhikevich), so inject
+    // a NaN conductance through the live mirror; it reaches v on the next advance.
+    sim.population_state("kc").gExc[3] = std::numeric_limits<scalar>::quiet_NaN();
+    sim.step();
+    const auto& st = sim.population_state("kc");
+    CHECK(st.nanFlag[3] == 1);
+    std::int64_t prev = st.flagged;
+    while (sim.steps_done() < sim.steps_total()) {
+        sim.step();
+        CHECK(st.flagged >= prev);
+        prev = st.flagged;
+    }
+    RunResult r = sim.finish();
+    CHECK(r.sumNaNs >= 1);
+
+    MBodyBuildOptions o2;
+    o2.dtMs = 0.1;
+    o2.durationMs = 100.0;
+    NetworkSpec net = build_mbody_net(100, 20, 2000, 100,
+                                      {{"pn_kc", 2.0}, {"pn_lhi", 1.0}, {"lhi_kc", 0.1},
+                                       {"kc_dn", 0.015}},
+                                      7, o2);
+    const std::string a = raster_to_csv(run(net, StorageMode::ForceDense).raster);
+    const std::string b = raster_to_csv(run(net, StorageMode::ForceSparse).raster);
+    const std::string c = raster_to_csv(run(net, StorageMode::FromSpec).raster);
+    CHECK(a == b);
+    CHECK(a == c);
+    CHECK(a.size() > 1000);
+}
+
+int main() {
+    conductance_kat();
+    propagate_examples();
+    fault_injection_and_storage();
+    if (failures) {
+        std::fprintf(stderr, "%d check(s) failed\n", failures);
+        return 1;
+    }
+    std::printf("facade tests passed\n");
+    return 0;
+}
