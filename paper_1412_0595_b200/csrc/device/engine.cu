@@ -29,6 +29,62 @@ void check(cudaError_t e, const char* what) {
 
 int round_up(int v, int u) { return (v + u - 1) / u * u; }
 
+// CRS tile pack of an inline sparse group for post tiles of tileN neurons
+// (layout in kernels.cuh, GroupDev::tpack).  With words == nullptr only the
+// largest tile's size (in 32-bit words, a multiple of 4) is computed.
+std::int64_t tile_pack(const HostGroup& g, int tileN, std::vector<std::uint32_t>* words,
+                       std::vector<long long>* off) {
+    const int nwT = tileN / 32;
+    const int nTiles = (g.nPost + tileN - 1) / tileN;
+    const int rows = g.preCount;
+    std::vector<std::int64_t> cur(g.rowStart, g.rowStart + rows);
+    std::int64_t maxWords = 0;
+    if (off) off->assign(1, 0);
+    for (int t = 0; t < nTiles; ++t) {
+        const int hiPost = static_cast<int>(std::min<std::int64_t>(
+            static_cast<std::int64_t>(t + 1) * tileN, g.nPost));
+        std::int64_t nnzTile = 0;
+        std::vector<std::int64_t> hi(rows);
+        for (int r = 0; r < rows; ++r) {
+            std::int64_t h = cur[r];
+            const std::int64_t end = g.rowStart[r + 1];
+            while (h < end && g.ind[h] < hiPost) ++h;
+            hi[r] = h;
+            nnzTile += h - cur[r];
+        }
+        const std::int64_t nw = (2LL * rows * nwT + nnzTile + 3) / 4 * 4;
+        maxWords = std::max(maxWords, nw);
+        if (words) {
+            const std::size_t base = words->size();
+            words->resize(base + nw, 0u);
+            std::uint32_t* M = words->data() + base;
+            std::uint32_t* Pf = M + static_cast<std::size_t>(rows) * nwT;
+            float* V = reinterpret_cast<float*>(Pf + static_cast<std::size_t>(rows) * nwT);
+            std::uint32_t vi = 0;
+            const int tile0 = t * tileN;
+            for (int r = 0; r < rows; ++r) {
+                std::uint32_t* m = M + static_cast<std::size_t>(r) * nwT;
+                for (std::int64_t q = cur[r]; q < hi[r]; ++q) {
+                    const int c = g.ind[q] - tile0;
+                    m[c >> 5] |= 1u << (c & 31);
+                }
+                std::uint32_t run = vi;
+                for (int k = 0; k < nwT; ++k) {
+                    Pf[static_cast<std::size_t>(r) * nwT + k] = run;
+                    run += static_cast<std::uint32_t>(__builtin_popcount(m[k]));
+                }
+                for (std::int64_t q = cur[r]; q < hi[r]; ++q) std::memcpy(V + vi++, g.g + q, 4);
+            }
+            off->push_back(static_cast<long long>(words->size()));
+        }
+        cur.swap(hi);
+    }
+    return maxWords;
+}
+
+// Largest tile pack (words) staged in shared memory.
+constexpr std::int64_t kTilePackMaxWords = 64 * 1024 / 4;
+
 }  // namespace
 
 int device_count() {
@@ -365,8 +421,10 @@ int DeviceEngine::Impl::plan_stage(const HostNet& net, int pi, int tileN, ssbk::
     const int W = Wmax;
     const bool single = P.n <= tileN;
     std::int64_t total = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-        const bool allowW = pass == 0;
+    for (int pass = 0; pass < 3; ++pass) {
+        // pass 0: stage dense weight tiles and CRS tile packs; 1: tile packs
+        // only; 2: neither (the fold reads them from L2)
+        const bool allowW = pass == 0, allowT = pass <= 1;
         std::int64_t off = 0;
         for (int a = 0; a < 2; ++a) {
             out[a] = ssbk::StageAcc{};
@@ -390,23 +448,31 @@ int DeviceEngine::Impl::plan_stage(const HostNet& net, int pi, int tileN, ssbk::
                         S.offW = static_cast<int>(off);
                         off += wbytes;
                     }
-                } else {
-                    S.offLo = static_cast<int>(off);
-                    off += static_cast<std::int64_t>(S.listCap) * 4;
-                    S.offEoff = static_cast<int>(off);
-                    off += static_cast<std::int64_t>(S.listCap + 1) * 4;
-                    const double perRow = g.preCount > 0 ? static_cast<double>(g.nnz) /
-                                                               g.preCount * tileN /
-                                                               std::max(1, g.nPost)
-                                                         : 0.0;
-                    S.entCap = static_cast<int>(std::min<double>(
-                        4096.0, std::max(512.0, S.listCap * (1.5 * perRow + 4.0))));
-                    S.offEidx = static_cast<int>(off);
-                    off += static_cast<std::int64_t>(S.entCap) * 2;
-                    off = align(off, 4);
-                    S.offEg = static_cast<int>(off);
-                    off += static_cast<std::int64_t>(S.entCap) * 4;
+                    continue;
                 }
+                const std::int64_t tw = allowT ? tile_pack(g, tileN, nullptr, nullptr) : 0;
+                if (allowT && tw <= kTilePackMaxWords) {
+                    S.tpackWords = static_cast<int>(std::max<std::int64_t>(tw, 4));
+                    off = align(off, 16);
+                    S.offT = static_cast<int>(off);
+                    off += static_cast<std::int64_t>(S.tpackWords) * 4;
+                    continue;
+                }
+                S.offLo = static_cast<int>(off);
+                off += static_cast<std::int64_t>(S.listCap) * 4;
+                S.offEoff = static_cast<int>(off);
+                off += static_cast<std::int64_t>(S.listCap + 1) * 4;
+                const double perRow = g.preCount > 0 ? static_cast<double>(g.nnz) /
+                                                           g.preCount * tileN /
+                                                           std::max(1, g.nPost)
+                                                     : 0.0;
+                S.entCap = static_cast<int>(std::min<double>(
+                    4096.0, std::max(512.0, S.listCap * (1.5 * perRow + 4.0))));
+                S.offEidx = static_cast<int>(off);
+                off += static_cast<std::int64_t>(S.entCap) * 2;
+                off = align(off, 4);
+                S.offEg = static_cast<int>(off);
+                off += static_cast<std::int64_t>(S.entCap) * 4;
             }
         }
         const std::int64_t inBudget =
@@ -625,6 +691,21 @@ void DeviceEngine::Impl::build(const HostNet& net) {
                 CK(cudaGetLastError());
             }
             G.seg = seg;
+            // static CRS tile pack when the post kernel's plan stages one
+            bool packed = false;
+            for (int a = 0; a < 2 && post.kind == kCondLif; ++a)
+                for (int k = 0; k < post.acc[a].ng; ++k)
+                    if (post.accGroups[a][k] == static_cast<int>(gi) &&
+                        post.stage[a].g[k].tpackWords > 0)
+                        packed = true;
+            if (packed) {
+                std::vector<std::uint32_t> words;
+                std::vector<long long> offs;
+                tile_pack(g, post.tileN, &words, &offs);
+                G.tpack = upload<std::uint32_t>(words.data(), words.size());
+                G.tpackOff = upload<long long>(offs.data(), offs.size());
+                G.nwT = post.tileN / 32;
+            }
         }
         HostGroup meta;
         meta.name = g.name;
