@@ -118,8 +118,8 @@ bool kernel_attributes(const std::string& name, int& regs, int& sharedBytes, int
     if (name == "condlif_window") e = cudaFuncGetAttributes(&a, ssbk::condlif_window_kernel);
     else if (name == "poisson_window") e = cudaFuncGetAttributes(&a, ssbk::poisson_window_kernel);
     else if (name == "dense_window") e = cudaFuncGetAttributes(&a, ssbk::dense_window_kernel);
-    else if (name == "dense_window_tma")
-        e = cudaFuncGetAttributes(&a, ssbk::dense_window_tma_kernel);
+    else if (name == "dense_window_warp")
+        e = cudaFuncGetAttributes(&a, ssbk::dense_window_warp_kernel);
     else if (name == "sparse_window") e = cudaFuncGetAttributes(&a, ssbk::sparse_window_kernel);
     else if (name == "compact_window") e = cudaFuncGetAttributes(&a, ssbk::compact_window_kernel);
     else if (name == "raster_window") e = cudaFuncGetAttributes(&a, ssbk::raster_window_kernel);
@@ -323,33 +323,33 @@ struct DeviceEngine::Impl {
     }
 
     static constexpr int kRowBlock = 128;
-    static int ring_smem(int bd, bool tma) {
-        return ssbk::kRingStages * ssbk::kRingRows * bd * 4 + (tma ? ssbk::kRingStages * 8 : 0) +
-               ssbk::kListSeg * 4;
+    static constexpr int kWarpRingBytes =
+        ssbk::kWarpStages * 32 * ssbk::kWarpRowStride * 4 + ssbk::kWarpListCap * 4;
+    static int ring_smem() {
+        return ssbk::kRingStages * ssbk::kRingRows * kRowBlock * 4 + ssbk::kListSeg * 4;
     }
     // Dense group inputs for window steps [wLo, wLo + nW): spiking rows
-    // streamed through shared memory (cp.async by default, TMA bulk copies
-    // with SSB_DENSE_KERNEL=tma) when they are 16-byte multiples, plain
-    // coalesced gathers otherwise.
-    bool useTma = false;
+    // streamed through shared memory when they are 16-byte multiples (one
+    // warp per step with a per-lane cp.async ring; SSB_DENSE_KERNEL=pipe
+    // selects the block-per-step ring), plain coalesced gathers otherwise.
+    bool usePipe = false;
     void launch_dense(const ssbk::GroupDev& G, const std::string& gname, const char* tag,
                       float* out, long long stride, int wLo, int nW, int first, cudaStream_t s) {
-        if (G.nPost % 4 == 0 && !useTma) {
+        if (G.nPost % 4 == 0 && !usePipe) {
+            dim3 grid((G.nPost + ssbk::kWarpSlab - 1) / ssbk::kWarpSlab, nW);
+            launch(std::string(tag) + gname, [&] {
+                ssbk::dense_window_warp_kernel<<<grid, 32, kWarpRingBytes, s>>>(G, out, stride,
+                                                                                 wLo, first);
+            });
+        } else if (G.nPost % 4 == 0) {
             dim3 grid((G.nPost + kRowBlock - 1) / kRowBlock, nW);
-            const bool wide = is_wide(static_cast<long long>(grid.x) * grid.y,
-                                      ring_smem(kRowBlock, false));
+            const bool wide = is_wide(static_cast<long long>(grid.x) * grid.y, ring_smem());
             if (wide) before_wide(s);
             launch(std::string(tag) + gname, [&] {
-                ssbk::dense_window_pipe_kernel<<<grid, kRowBlock, ring_smem(kRowBlock, false), s>>>(
+                ssbk::dense_window_pipe_kernel<<<grid, kRowBlock, ring_smem(), s>>>(
                     G, out, stride, wLo, first);
             });
             if (wide) after_wide(s);
-        } else if (G.nPost % 4 == 0) {
-            dim3 grid((G.nPost + kRowBlock - 1) / kRowBlock, nW);
-            launch(std::string(tag) + gname, [&] {
-                ssbk::dense_window_tma_kernel<<<grid, kRowBlock, ring_smem(kRowBlock, true), s>>>(
-                    G, out, stride, wLo, first);
-            });
         } else {
             dim3 grid((G.nPost + 127) / 128, nW);
             launch(std::string(tag) + gname, [&] {
@@ -781,11 +781,11 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     for (const auto& P : pops) maxSmem = std::max(maxSmem, P.smemBytes);
     CK(cudaFuncSetAttribute(ssbk::condlif_window_kernel,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(maxSmem, 4096)));
-    CK(cudaFuncSetAttribute(ssbk::dense_window_tma_kernel,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, ring_smem(kRowBlock, true)));
+    CK(cudaFuncSetAttribute(ssbk::dense_window_warp_kernel,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpRingBytes));
     CK(cudaFuncSetAttribute(ssbk::dense_window_pipe_kernel,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, ring_smem(kRowBlock, false)));
-    if (const char* e = std::getenv("SSB_DENSE_KERNEL")) useTma = std::string(e) == "tma";
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, ring_smem()));
+    if (const char* e = std::getenv("SSB_DENSE_KERNEL")) usePipe = std::string(e) == "pipe";
     CK(cudaFuncSetAttribute(ssbk::sparse_window_kernel,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 4));
     CK(cudaStreamSynchronize(stream));
