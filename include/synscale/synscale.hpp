@@ -303,7 +303,16 @@ struct EngineOptions {
     std::int64_t rasterCapacity = 0;
     bool profile = false;
     bool forceStepMode = false;
+    // multi-GPU (one process per GPU): rank of world, NCCL id from
+    // comm_unique_id() on rank 0 shared by the caller; virtualWorld > 1 runs
+    // that many shards in this process on one GPU instead
+    int rank = 0, world = 1, virtualWorld = 0, shardMinSize = 0;
+    bool hasCommId = false;
+    std::array<unsigned char, 128> commId{};
 };
+
+// NCCL unique id for EngineOptions::commId (B200 extension).
+std::array<unsigned char, 128> comm_unique_id();
 
 class Simulation {
 public:

@@ -132,6 +132,18 @@ typedef struct ssb_engine_opts {
     int64_t raster_capacity;     /* events kept on device between host flushes */
     int32_t profile;             /* 1 = time every launch with CUDA events */
     int32_t force_step_mode;     /* 1 = never fuse steps (window forced to 1) */
+    /* multi-GPU: one process per GPU, rank of world_size, NCCL
+     * communicator from comm_id (ssb_comm_unique_id on rank 0, broadcast by
+     * the caller).  CondLif populations of >= shard_min_size neurons are split
+     * by neuron ranges; each window's spike bitmasks are all-gathered.
+     * virtual_world > 1 instead runs that many shards in this process on one
+     * GPU (exchange by device copies; for testing the split path). */
+    int32_t rank;
+    int32_t world_size;          /* 0 or 1 = single GPU */
+    int32_t virtual_world;
+    int32_t shard_min_size;      /* 0 = default (64) */
+    int32_t has_comm_id;
+    uint8_t comm_id[128];
 } ssb_engine_opts;
 
 /* Result summary (RunResult, engine.hpp:35-42). */
@@ -212,6 +224,22 @@ SSB_API int ssb_build_group(const ssb_net_desc* net, int32_t storage_mode, int32
                             float* values, int32_t* post_ind, int64_t* row_start, int64_t cap,
                             char* err, size_t errlen);
 SSB_API uint64_t ssb_mem_sparse_elements(uint64_t nnz, uint64_t n_post); /* matrix.cpp:176 */
+
+/* ---- multi-GPU decomposition (host, no GPU needed) ------------------------- */
+/* Neuron ranges of a world of `world` ranks: bounds[p*(world+1) + r] = first
+ * neuron of rank r in population p (r = world: the size), or -1 for every r
+ * when population p is whole (replicated).  SpecError for recurrent nets. */
+SSB_API int ssb_shard_plan(const ssb_net_desc* net, int32_t world, int32_t min_size,
+                           int64_t* bounds, char* err, size_t errlen);
+/* Group `group` as rank `rank` holds it (ssb_build_group of the column slice
+ * of a split post population; n_post = the local column count). */
+SSB_API int ssb_shard_group(const ssb_net_desc* net, int32_t storage_mode, int32_t group,
+                            int32_t world, int32_t rank, int32_t min_size, int32_t* storage,
+                            int32_t* n_pre, int32_t* n_post, int64_t* nnz, float* values,
+                            int32_t* post_ind, int64_t* row_start, int64_t cap, char* err,
+                            size_t errlen);
+/* NCCL unique id for ssb_engine_opts.comm_id (loads libnccl; no GPU work). */
+SSB_API int ssb_comm_unique_id(uint8_t* out128, char* err, size_t errlen);
 SSB_API uint64_t ssb_mem_dense_elements(uint64_t n_pre, uint64_t n_post); /* matrix.cpp:180 */
 
 /* ---- standalone device kernels -------------------------------------------- */
@@ -253,6 +281,11 @@ SSB_API const char* ssb_last_error(const ssb_sim* sim);
  * SSB_ERR_SPEC when finished or when fewer than n steps remain. */
 SSB_API int ssb_step(ssb_sim* sim, int64_t n);
 SSB_API int64_t ssb_steps_total(const ssb_sim* sim);
+/* Ranks the network is split over and this process's range of population
+ * `pop`: neurons [lo, lo + n_local) of n_global. */
+SSB_API int32_t ssb_world(const ssb_sim* sim);
+SSB_API int ssb_shard_range(const ssb_sim* sim, int32_t pop, int64_t* lo, int64_t* n_local,
+                            int64_t* n_global);
 SSB_API int64_t ssb_steps_done(const ssb_sim* sim);
 /* Waits for all queued work of the handle. */
 SSB_API int ssb_sync(ssb_sim* sim);

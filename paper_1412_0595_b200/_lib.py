@@ -73,6 +73,9 @@ class ssb_engine_opts(C.Structure):
         ("block_policy", C.c_int32), ("use_graphs", C.c_int32),
         ("heavy_pre_threshold", C.c_int32), ("raster_capacity", C.c_int64),
         ("profile", C.c_int32), ("force_step_mode", C.c_int32),
+        ("rank", C.c_int32), ("world_size", C.c_int32), ("virtual_world", C.c_int32),
+        ("shard_min_size", C.c_int32), ("has_comm_id", C.c_int32),
+        ("comm_id", C.c_uint8 * 128),
     ]
 
 
@@ -124,6 +127,10 @@ _SIGNATURES = {
                                           P(_f32), _cp, _sz]),
     "ssb_build_group": (C.c_int, [P(ssb_net_desc), _i32, _i32, P(_i32), P(_i32), P(_i32), P(_i64),
                                   P(_f32), P(_i32), P(_i64), _i64, _cp, _sz]),
+    "ssb_shard_plan": (C.c_int, [P(ssb_net_desc), _i32, _i32, P(_i64), _cp, _sz]),
+    "ssb_shard_group": (C.c_int, [P(ssb_net_desc), _i32, _i32, _i32, _i32, _i32, P(_i32), P(_i32),
+                                  P(_i32), P(_i64), P(_f32), P(_i32), P(_i64), _i64, _cp, _sz]),
+    "ssb_comm_unique_id": (C.c_int, [P(_u8), _cp, _sz]),
     "ssb_mem_sparse_elements": (_u64, [_u64, _u64]),
     "ssb_mem_dense_elements": (_u64, [_u64, _u64]),
     "ssb_propagate_dense": (C.c_int, [P(_f32), _i32, _i32, P(_i32), _i64, P(_f32), _i64, _cp, _sz]),
@@ -139,6 +146,8 @@ _SIGNATURES = {
     "ssb_last_error": (_cp, [_vp]),
     "ssb_step": (C.c_int, [_vp, _i64]),
     "ssb_steps_total": (_i64, [_vp]),
+    "ssb_world": (_i32, [_vp]),
+    "ssb_shard_range": (C.c_int, [_vp, _i32, P(_i64), P(_i64), P(_i64)]),
     "ssb_steps_done": (_i64, [_vp]),
     "ssb_sync": (C.c_int, [_vp]),
     "ssb_pull_state": (C.c_int, [_vp, _i32, _i32, _vp, _i64]),

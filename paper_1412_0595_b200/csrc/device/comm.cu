@@ -1,0 +1,89 @@
+// comm.cu — NCCL through dlopen (see comm.hpp).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../engine.hpp"
+#include "comm.hpp"
+
+namespace ssb {
+
+namespace {
+
+struct Nccl {
+    void* lib = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+Nccl& nccl() {
+    static Nccl n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            n.lib = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (n.lib) break;
+        }
+        if (!n.lib) return;
+        n.getUniqueId = reinterpret_cast<decltype(n.getUniqueId)>(dlsym(n.lib, "ncclGetUniqueId"));
+        n.commInitRank = reinterpret_cast<decltype(n.commInitRank)>(dlsym(n.lib, "ncclCommInitRank"));
+        n.commDestroy = reinterpret_cast<decltype(n.commDestroy)>(dlsym(n.lib, "ncclCommDestroy"));
+        n.allGather = reinterpret_cast<decltype(n.allGather)>(dlsym(n.lib, "ncclAllGather"));
+        n.allReduce = reinterpret_cast<decltype(n.allReduce)>(dlsym(n.lib, "ncclAllReduce"));
+        n.errorString = reinterpret_cast<decltype(n.errorString)>(dlsym(n.lib, "ncclGetErrorString"));
+    });
+    if (!n.lib || !n.getUniqueId || !n.commInitRank || !n.allGather || !n.allReduce)
+        throw DeviceError("NCCL (libnccl.so.2) is not available for a multi-GPU run");
+    return n;
+}
+
+void nck(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw DeviceError(std::string("NCCL error in ") + what + ": " +
+                          (nccl().errorString ? nccl().errorString(r) : std::to_string(r)));
+}
+
+}  // namespace
+
+std::array<unsigned char, 128> nccl_unique_id() {
+    ncclUniqueId id;
+    nck(nccl().getUniqueId(&id), "ncclGetUniqueId");
+    std::array<unsigned char, 128> out{};
+    std::memcpy(out.data(), id.internal, 128);
+    return out;
+}
+
+std::array<unsigned char, 128> comm_unique_id() { return nccl_unique_id(); }
+
+Comm::Comm(int world, int rank, const unsigned char* id128) : world_(world), rank_(rank) {
+    ncclUniqueId id;
+    std::memcpy(id.internal, id128, 128);
+    ncclComm_t c = nullptr;
+    nck(nccl().commInitRank(&c, world, id, rank), "ncclCommInitRank");
+    comm_ = c;
+}
+
+Comm::~Comm() {
+    if (comm_ && nccl().commDestroy) nccl().commDestroy(static_cast<ncclComm_t>(comm_));
+}
+
+void Comm::allgather_u32(const void* send, void* recv, std::size_t count, cudaStream_t s) {
+    nck(nccl().allGather(send, recv, count, ncclUint32, static_cast<ncclComm_t>(comm_), s),
+        "ncclAllGather");
+}
+
+void Comm::allreduce_sum_u64(void* buf, std::size_t count, cudaStream_t s) {
+    nck(nccl().allReduce(buf, buf, count, ncclUint64, ncclSum, static_cast<ncclComm_t>(comm_), s),
+        "ncclAllReduce");
+}
+
+}  // namespace ssb

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../engine.hpp"
+#include "comm.hpp"
 #include "kernels.cuh"
 #include "synscale/synscale.hpp"
 
@@ -157,6 +158,14 @@ struct DeviceEngine::Impl {
         int offIn = 0;              // shared offset of the phase-A inputs
         std::vector<int> accGroups[2];  // group indices in spec order
         std::string name;
+        // split population (multi-GPU): the kernel advances the local range
+        // [lo, lo + n) into kdev[b] (local bits, stride nwords = chunk words);
+        // the exchange gathers every rank's bits and devb[b] holds the global
+        // bits / lists (n = nGlobal) that consumers and the raster read.
+        bool sharded = false;
+        int nGlobal = 0, lo = 0, shardChunk = 0, nwGlobal = 0;
+        ssbk::PopDev kdev[2]{};
+        uint32_t* gathered[2] = {nullptr, nullptr};  // [world][W][nwords]
     };
     struct LaunchStat {
         std::string name;
@@ -165,6 +174,20 @@ struct DeviceEngine::Impl {
     };
 
     EngineConfig cfg;
+    int world = 1;              // ranks (or virtual shards) the network is split over
+    bool virtualShard = false;  // one of several shards in this process (exchange by copies)
+    bool serial = false;        // one stream, no graphs (profiling, virtual shards)
+    bool ownsStream = true;
+    std::unique_ptr<Comm> comm;  // NCCL, one process per GPU
+    char* commScratch = nullptr;  // state gathers of split populations
+    std::size_t commScratchBytes = 0;
+    char* comm_scratch(std::size_t bytes) {
+        if (bytes > commScratchBytes) {
+            commScratch = alloc<char>(bytes);
+            commScratchBytes = bytes;
+        }
+        return commScratch;
+    }
     int Wmax = 1;
     bool stepMode = false;
     int smCount = 148;
@@ -283,6 +306,9 @@ struct DeviceEngine::Impl {
                    int& C, int& offBits) const;
     void build(const HostNet& net);
     void enqueue_pop(int pi, int W, int b, cudaStream_t s);
+    void assemble_compact(int pi, int W, int b, cudaStream_t s);
+    std::int64_t pre_launch(int W, int M);
+    void post_launch(int W, int M, std::int64_t add);
     void enqueue_tail(int W, int b, cudaStream_t s);
     void enqueue_windows(int W, int M);
     void run_windows(int W, int M);
@@ -546,8 +572,14 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         P.kind = hp.kind;
         P.n = hp.n;
         P.name = hp.name;
-        P.nwords = (hp.n + 31) / 32;
-        totalNeurons += hp.n;
+        P.sharded = hp.nGlobal > 0;
+        P.nGlobal = P.sharded ? hp.nGlobal : hp.n;
+        P.lo = hp.lo;
+        P.shardChunk = hp.chunk;
+        P.nwGlobal = (P.nGlobal + 31) / 32;
+        // kernel-side bitmask stride: a split population sends equal slices
+        P.nwords = P.sharded ? (hp.chunk + 31) / 32 : (hp.n + 31) / 32;
+        totalNeurons += P.nGlobal;
         for (int a = 0; a < 2; ++a) {
             auto& A = P.acc[a];
             const auto& gl = P.accGroups[a];
@@ -648,6 +680,21 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             if (P.acc[a].mode == ssbk::kAccBuffered)
                 P.accb[1][a].buf = alloc<float>(static_cast<std::size_t>(Wmax + 1) * n);
         }
+        P.kdev[0] = P.devb[0];
+        P.kdev[1] = P.devb[1];
+        if (P.sharded) {
+            const std::size_t ng = static_cast<std::size_t>(P.nGlobal);
+            for (int b = 0; b < 2; ++b) {
+                P.gathered[b] = alloc<uint32_t>(static_cast<std::size_t>(world) * Wmax * P.nwords);
+                auto& g = P.devb[b];
+                g.n = P.nGlobal;
+                g.nwords = P.nwGlobal;
+                g.bits = alloc<uint32_t>(static_cast<std::size_t>(Wmax) * P.nwGlobal);
+                g.list = alloc<int>(static_cast<std::size_t>(Wmax) * ng);
+                g.count = alloc<int>(static_cast<std::size_t>(Wmax));
+            }
+            P.dev.n = P.n;
+        }
     }
     for (const auto& g : net.groups) {
         if (stepMode || net.pops[g.post].kind == kPoisson) continue;  // inputs via state
@@ -670,7 +717,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         G.nPost = g.nPost;
         G.preOffset = g.preOffset;
         G.preCount = g.preCount;
-        G.preN = pre.n;
+        G.preN = pre.nGlobal;  // the pre population's (global) spike list stride
         G.preList = pre.dev.list;
         G.preCnt = pre.dev.count;
         if (g.dense) {
@@ -732,7 +779,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     // raster arena
     raster.nPops = nPops;
     for (int pi = 0; pi < nPops; ++pi) {
-        raster.n[pi] = pops[pi].n;
+        raster.n[pi] = pops[pi].nGlobal;
         raster.count[pi] = pops[pi].dev.count;
         raster.list[pi] = pops[pi].dev.list;
     }
@@ -776,18 +823,21 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     auxStreams.resize(nPops + 1);
     for (auto& s : auxStreams) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
 
-    // kernels with large dynamic shared tiles
+    // kernels with large dynamic shared tiles (the limit is per function and
+    // process-wide: only ever raised, several engines may share a device)
     int maxSmem = 0;
     for (const auto& P : pops) maxSmem = std::max(maxSmem, P.smemBytes);
-    CK(cudaFuncSetAttribute(ssbk::condlif_window_kernel,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(maxSmem, 4096)));
-    CK(cudaFuncSetAttribute(ssbk::dense_window_warp_kernel,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpRingBytes));
-    CK(cudaFuncSetAttribute(ssbk::dense_window_pipe_kernel,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, ring_smem()));
+    auto allow = [](const void* fn, int bytes) {
+        cudaFuncAttributes fa;
+        CK(cudaFuncGetAttributes(&fa, fn));
+        if (fa.maxDynamicSharedSizeBytes < bytes)
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    };
+    allow(reinterpret_cast<const void*>(&ssbk::condlif_window_kernel), std::max(maxSmem, 4096));
+    allow(reinterpret_cast<const void*>(&ssbk::dense_window_warp_kernel), kWarpRingBytes);
+    allow(reinterpret_cast<const void*>(&ssbk::dense_window_pipe_kernel), ring_smem());
+    allow(reinterpret_cast<const void*>(&ssbk::sparse_window_kernel), 4096 * 4);
     if (const char* e = std::getenv("SSB_DENSE_KERNEL")) usePipe = std::string(e) == "pipe";
-    CK(cudaFuncSetAttribute(ssbk::sparse_window_kernel,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 4));
     CK(cudaStreamSynchronize(stream));
 }
 
@@ -804,38 +854,63 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t s) {
         });
         return;
     }
-    for (int a = 0; a < 2; ++a) {
-        const auto& A = P.accb[b][a];
-        if (A.mode != ssbk::kAccBuffered) continue;
-        for (int k = 0; k < A.ng; ++k) {
-            const auto& G = A.g[k];
-            const int gi = P.accGroups[a][k];
-            float* out = A.buf + P.n;  // row w = 1
-            if (G.dense) {
-                launch_dense(G, groupMeta[gi].name, "dense_window:", out, P.n, 1, W, k == 0, s);
-            } else {
-                dim3 grid(G.nTiles, W);
-                launch("sparse_window:" + groupMeta[gi].name, [&] {
-                    ssbk::sparse_window_kernel<<<grid, G.segTile, G.segTile * 4, s>>>(G, out, P.n, 1,
-                                                                                     k == 0);
-                });
+    if (P.n > 0) {
+        for (int a = 0; a < 2; ++a) {
+            const auto& A = P.accb[b][a];
+            if (A.mode != ssbk::kAccBuffered) continue;
+            for (int k = 0; k < A.ng; ++k) {
+                const auto& G = A.g[k];
+                const int gi = P.accGroups[a][k];
+                float* out = A.buf + P.n;  // row w = 1
+                if (G.dense) {
+                    launch_dense(G, groupMeta[gi].name, "dense_window:", out, P.n, 1, W, k == 0, s);
+                } else {
+                    dim3 grid(G.nTiles, W);
+                    launch("sparse_window:" + groupMeta[gi].name, [&] {
+                        ssbk::sparse_window_kernel<<<grid, G.segTile, G.segTile * 4, s>>>(
+                            G, out, P.n, 1, k == 0);
+                    });
+                }
             }
         }
-    }
-    const bool wide = is_wide(P.grid, P.smemBytes);
-    if (wide) before_wide(s);
-    launch("condlif_window:" + P.name, [&] {
-        ssbk::condlif_window_kernel<<<P.grid, P.block, P.smemBytes, s>>>(
-            D, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk, P.offIn,
-            P.offBits);
-    });
-    if (P.grid > 1) {
-        const int bs = std::min(1024, round_up(P.nwords, 32));
-        launch("compact_window:" + P.name, [&] {
-            ssbk::compact_window_kernel<<<W, bs, 0, s>>>(D.bits, P.nwords, P.n, D.list, D.count);
+        const ssbk::PopDev& K = P.kdev[b];
+        const bool wide = is_wide(P.grid, P.smemBytes);
+        if (wide) before_wide(s);
+        launch("condlif_window:" + P.name, [&] {
+            ssbk::condlif_window_kernel<<<P.grid, P.block, P.smemBytes, s>>>(
+                K, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk,
+                P.offIn, P.offBits);
         });
+        if (P.grid > 1 && !P.sharded) {
+            const int bs = std::min(1024, round_up(P.nwords, 32));
+            launch("compact_window:" + P.name, [&] {
+                ssbk::compact_window_kernel<<<W, bs, 0, s>>>(K.bits, P.nwords, P.n, K.list, K.count);
+            });
+        }
+        if (wide) after_wide(s);
     }
-    if (wide) after_wide(s);
+    if (P.sharded) {
+        // the window's exchange: every rank's local bits, in rank order
+        if (comm)
+            comm->allgather_u32(P.kdev[b].bits, P.gathered[b],
+                                static_cast<std::size_t>(W) * P.nwords, s);
+        if (!virtualShard) assemble_compact(pi, W, b, s);  // virtual: after the shard copies
+    }
+}
+
+// Global bitmask and ordered spike lists of a split population from the
+// gathered local bitmasks (rank order = ascending neuron order).
+void DeviceEngine::Impl::assemble_compact(int pi, int W, int b, cudaStream_t s) {
+    auto& P = pops[pi];
+    const ssbk::PopDev& D = P.devb[b];
+    const int bs = std::min(1024, round_up(P.nwGlobal, 32));
+    launch("assemble_bits:" + P.name, [&] {
+        ssbk::assemble_bits_kernel<<<W, bs, 0, s>>>(P.gathered[b], W, P.nwords, P.shardChunk,
+                                                    P.nGlobal, P.nwGlobal, D.bits);
+    });
+    launch("compact_window:" + P.name, [&] {
+        ssbk::compact_window_kernel<<<W, bs, 0, s>>>(D.bits, P.nwGlobal, P.nGlobal, D.list, D.count);
+    });
 }
 
 // Accumulators written after every population advanced (cyclic graphs,
@@ -875,7 +950,7 @@ void DeviceEngine::Impl::enqueue_tail(int W, int b, cudaStream_t s) {
 // window m, and kc_dn / DN of window m overlap KC of window m+1.
 void DeviceEngine::Impl::enqueue_windows(int W, int M) {
     const int nPops = static_cast<int>(pops.size());
-    const bool multi = !cfg.profile;  // profile mode: one stream, serial order
+    const bool multi = !cfg.profile && !serial;  // profile / virtual shards: one stream
     const int rs = nPops;
     auto S = [&](int idx) { return multi ? auxStreams[idx] : stream; };
     evUsed = 0;
@@ -967,9 +1042,11 @@ void DeviceEngine::Impl::flush_raster(bool wait) {
     knownWin = epochStart = launchesDone;
 }
 
-void DeviceEngine::Impl::run_windows(int W, int M) {
+// Raster bookkeeping before a launch of M windows: learns the cursor of the
+// launch kRing back and flushes the arena if the worst case may overflow it.
+// Returns the launch's worst-case event count.
+std::int64_t DeviceEngine::Impl::pre_launch(int W, int M) {
     const std::int64_t add = static_cast<std::int64_t>(W) * M * totalNeurons;
-    // learn the cursor after the launch kRing back (bounds the host's run-ahead)
     if (launchesDone - kRing >= std::max(epochStart, knownWin)) {
         const std::int64_t idx = launchesDone - kRing;
         CK(cudaEventSynchronize(ringEv[idx % kRing]));
@@ -979,8 +1056,24 @@ void DeviceEngine::Impl::run_windows(int W, int M) {
     std::int64_t bound = knownCursor + add;
     for (std::int64_t l = knownWin; l < launchesDone; ++l) bound += ringAdd[l % kRing];
     if (bound > rasterCap) flush_raster();
+    return add;
+}
+
+void DeviceEngine::Impl::post_launch(int W, int M, std::int64_t add) {
+    windowsLaunched += M;
+    stepsDone += static_cast<std::int64_t>(W) * M;
+    const int slot = static_cast<int>(launchesDone % kRing);
+    CK(cudaMemcpyAsync(ringVal + slot, raster.cursor + (windowsLaunched & 1), sizeof(long long),
+                       cudaMemcpyDeviceToHost, stream));
+    CK(cudaEventRecord(ringEv[slot], stream));
+    ringAdd[slot] = add;
+    ++launchesDone;
+}
+
+void DeviceEngine::Impl::run_windows(int W, int M) {
+    const std::int64_t add = pre_launch(W, M);
     const int key = W * 64 + M;
-    if (cfg.useGraphs && !cfg.profile) {
+    if (cfg.useGraphs && !cfg.profile && !serial) {
         auto it = graphs.find(key);
         if (it == graphs.end()) {
             cudaGraph_t g;
@@ -1002,34 +1095,105 @@ void DeviceEngine::Impl::run_windows(int W, int M) {
         kernelLaunches += enqueued;
         harvest();
     }
-    windowsLaunched += M;
-    stepsDone += static_cast<std::int64_t>(W) * M;
-    const int slot = static_cast<int>(launchesDone % kRing);
-    CK(cudaMemcpyAsync(ringVal + slot, raster.cursor + (windowsLaunched & 1), sizeof(long long),
-                       cudaMemcpyDeviceToHost, stream));
-    CK(cudaEventRecord(ringEv[slot], stream));
-    ringAdd[slot] = add;
-    ++launchesDone;
+    post_launch(W, M, add);
 }
 
 // ---------------------------------------------------------------------------
 
-DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfg)
+DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfgIn)
     : impl_(std::make_unique<Impl>()) {
-    auto& m = *impl_;
-    m.cfg = cfg;
-    if (m.cfg.heavyPreThreshold <= 0) m.cfg.heavyPreThreshold = 1024;
-    if (m.cfg.window <= 0) m.cfg.window = 64;
+    EngineConfig cfg = cfgIn;
+    if (cfg.heavyPreThreshold <= 0) cfg.heavyPreThreshold = 1024;
+    if (cfg.window <= 0) cfg.window = 64;
     if (device_count() == 0) throw DeviceError("no CUDA device is visible (the engine has no CPU path)");
     CK(cudaSetDevice(cfg.device));
-    m.smCount = device_props(cfg.device).smCount;
-    CK(cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking));
-    try {
-        m.build(net);
-    } catch (...) {
-        m.release();
-        throw;
+    const bool virt = cfg.virtualWorld > 1;
+    const int R = virt ? cfg.virtualWorld : std::max(1, cfg.world);
+    if (!virt && R > 1 && !cfg.hasCommId)
+        throw synscale::SpecError("a multi-GPU run needs a communicator id (ssb_comm_unique_id)");
+    if (!virt && R > 1 && (cfg.rank < 0 || cfg.rank >= R))
+        throw synscale::SpecError("rank " + std::to_string(cfg.rank) + " outside a world of " +
+                                  std::to_string(R));
+    const ShardPlan plan = R > 1 ? plan_shards(net, R, cfg.shardMinSize) : ShardPlan{};
+    const int smCount = device_props(cfg.device).smCount;
+    auto init = [&](Impl& m, int rank, cudaStream_t shared) {
+        m.cfg = cfg;
+        m.cfg.rank = rank;
+        m.world = R;
+        m.smCount = smCount;
+        m.virtualShard = virt;
+        if (virt) {  // lockstep across shards on one stream
+            m.serial = true;
+            m.cfg.useGraphs = false;
+        }
+        if (shared) {
+            m.stream = shared;
+            m.ownsStream = false;
+        } else {
+            CK(cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking));
+        }
+        try {
+            ShardStore store;
+            const HostNet local = R > 1 ? shard_net(net, plan, rank, store) : HostNet{};
+            if (R > 1 && !virt) m.comm = std::make_unique<Comm>(R, rank, cfg.commId.data());
+            m.build(R > 1 ? local : net);
+        } catch (...) {
+            m.release();
+            throw;
+        }
+    };
+    init(*impl_, virt ? 0 : (R > 1 ? cfg.rank : 0), nullptr);
+    if (virt) {
+        try {
+            for (int r = 1; r < R; ++r) {
+                shards_.push_back(std::make_unique<Impl>());
+                init(*shards_.back(), r, impl_->stream);
+                shards_.back()->rasterDiscarded = true;  // shard 0 keeps the (identical) raster
+            }
+        } catch (...) {
+            for (auto& sh : shards_) sh->release();
+            shards_.clear();
+            impl_->release();
+            throw;
+        }
     }
+}
+
+// Virtual shards: window W of every shard on the shared stream, population by
+// population in topological order; a split population's local bitmasks are
+// copied into every shard's gather buffer (the all-gather of a real world)
+// before each shard assembles its global lists.
+void DeviceEngine::lockstep(int W) {
+    std::vector<Impl*> all{impl_.get()};
+    for (auto& sh : shards_) all.push_back(sh.get());
+    const int R = static_cast<int>(all.size());
+    std::vector<std::int64_t> add(R);
+    for (int r = 0; r < R; ++r) add[r] = all[r]->pre_launch(W, 1);
+    Impl& m0 = *impl_;
+    const int b = static_cast<int>(m0.windowsLaunched & 1);
+    for (auto* m : all) {
+        m->enqueued = 0;
+        m->evUsed = 0;
+        m->multiStream = false;
+        m->lastWide = nullptr;
+    }
+    for (int pi : m0.order) {
+        for (auto* m : all) m->enqueue_pop(pi, W, b, m0.stream);
+        if (!m0.pops[pi].sharded) continue;
+        const std::size_t words = static_cast<std::size_t>(W) * m0.pops[pi].nwords;
+        for (int src = 0; src < R; ++src)
+            for (int dst = 0; dst < R; ++dst)
+                CK(cudaMemcpyAsync(all[dst]->pops[pi].gathered[b] + src * words,
+                                   all[src]->pops[pi].kdev[b].bits, words * 4,
+                                   cudaMemcpyDeviceToDevice, m0.stream));
+        for (auto* m : all) m->assemble_compact(pi, W, b, m0.stream);
+    }
+    for (auto* m : all) {
+        m->enqueue_tail(W, b, m0.stream);
+        m->kernelLaunches += m->enqueued;
+        m->harvest();
+    }
+    for (int r = 0; r < R; ++r) all[r]->post_launch(W, 1, add[r]);
 }
 
 void DeviceEngine::Impl::release() {
@@ -1056,17 +1220,28 @@ void DeviceEngine::Impl::release() {
     allocations.clear();
     for (cudaStream_t s : auxStreams) cudaStreamDestroy(s);
     auxStreams.clear();
-    if (stream) cudaStreamDestroy(stream), stream = nullptr;
+    comm.reset();
+    if (stream && ownsStream) cudaStreamDestroy(stream);
+    stream = nullptr;
 }
 
 DeviceEngine::~DeviceEngine() {
     cudaSetDevice(impl_->cfg.device);
+    for (auto& sh : shards_) sh->release();  // they borrow shard 0's stream
     impl_->release();
 }
 
 void DeviceEngine::step(std::int64_t n) {
     auto& m = *impl_;
     CK(cudaSetDevice(m.cfg.device));
+    if (!shards_.empty()) {
+        while (n > 0) {
+            const int W = static_cast<int>(std::min<std::int64_t>(m.Wmax, n));
+            lockstep(W);
+            n -= W;
+        }
+        return;
+    }
     const std::int64_t full = static_cast<std::int64_t>(m.Wmax) * m.graphWindows;
     while (n > 0) {
         if (m.graphWindows > 1 && n >= full) {
@@ -1104,6 +1279,17 @@ void* field_ptr(const ssbk::PopDev& d, int field, std::size_t& esz) {
 }
 }  // namespace
 
+// State of a split population is assembled to the whole population on the
+// way out and split on the way in, so callers see the unsplit engine: a
+// real world all-gathers the chunk-padded local slices over NCCL, virtual
+// shards are read one by one.  FLAGGED (the NaN counter) is summed.
+namespace {
+struct Slice {
+    void* ptr;
+    std::size_t esz;
+};
+}  // namespace
+
 void DeviceEngine::pull(int pop, int field, void* dst, std::int64_t count) {
     auto& m = *impl_;
     CK(cudaSetDevice(m.cfg.device));
@@ -1111,7 +1297,55 @@ void DeviceEngine::pull(int pop, int field, void* dst, std::int64_t count) {
     void* src = field_ptr(m.pops.at(pop).dev, field, esz);
     if (!src) throw synscale::SpecError("unknown state field " + std::to_string(field));
     CK(cudaStreamSynchronize(m.stream));
-    CK(cudaMemcpy(dst, src, esz * static_cast<std::size_t>(count), cudaMemcpyDeviceToHost));
+    const auto& P = m.pops.at(pop);
+    if (!P.sharded) {
+        CK(cudaMemcpy(dst, src, esz * static_cast<std::size_t>(count), cudaMemcpyDeviceToHost));
+        return;
+    }
+    if (field == kFieldFlagged) {
+        unsigned long long total = 0, part = 0;
+        if (!shards_.empty()) {
+            CK(cudaMemcpy(&total, P.dev.flagged, 8, cudaMemcpyDeviceToHost));
+            for (auto& sh : shards_) {
+                CK(cudaMemcpy(&part, sh->pops.at(pop).dev.flagged, 8, cudaMemcpyDeviceToHost));
+                total += part;
+            }
+        } else {
+            auto* tmp = reinterpret_cast<unsigned long long*>(m.comm_scratch(8));
+            CK(cudaMemcpyAsync(tmp, P.dev.flagged, 8, cudaMemcpyDeviceToDevice, m.stream));
+            m.comm->allreduce_sum_u64(tmp, 1, m.stream);
+            CK(cudaStreamSynchronize(m.stream));
+            CK(cudaMemcpy(&total, tmp, 8, cudaMemcpyDeviceToHost));
+        }
+        std::memcpy(dst, &total, 8);
+        return;
+    }
+    const std::int64_t n = std::min<std::int64_t>(count, P.nGlobal);
+    char* out = static_cast<char*>(dst);
+    if (!shards_.empty()) {
+        for (Impl* sh : [&] {
+                 std::vector<Impl*> v{impl_.get()};
+                 for (auto& x : shards_) v.push_back(x.get());
+                 return v;
+             }()) {
+            const auto& Q = sh->pops.at(pop);
+            std::size_t e2;
+            void* s2 = field_ptr(Q.dev, field, e2);
+            const std::int64_t k = std::max<std::int64_t>(0, std::min<std::int64_t>(Q.n, n - Q.lo));
+            if (k > 0)
+                CK(cudaMemcpy(out + esz * Q.lo, s2, esz * k, cudaMemcpyDeviceToHost));
+        }
+        return;
+    }
+    // one process per GPU: all-gather chunk-padded slices (chunk*esz is a
+    // multiple of 4 bytes: chunks are multiples of 4 neurons)
+    const std::size_t sliceBytes = esz * static_cast<std::size_t>(P.shardChunk);
+    char* send = m.comm_scratch(sliceBytes * (m.world + 1));
+    char* recv = send + sliceBytes;
+    if (P.n) CK(cudaMemcpyAsync(send, src, esz * P.n, cudaMemcpyDeviceToDevice, m.stream));
+    m.comm->allgather_u32(send, recv, sliceBytes / 4, m.stream);
+    CK(cudaStreamSynchronize(m.stream));
+    CK(cudaMemcpy(out, recv, esz * n, cudaMemcpyDeviceToHost));
 }
 
 void DeviceEngine::push(int pop, int field, const void* src, std::int64_t count) {
@@ -1121,8 +1355,38 @@ void DeviceEngine::push(int pop, int field, const void* src, std::int64_t count)
     void* dst = field_ptr(m.pops.at(pop).dev, field, esz);
     if (!dst) throw synscale::SpecError("unknown state field " + std::to_string(field));
     CK(cudaStreamSynchronize(m.stream));
-    CK(cudaMemcpy(dst, src, esz * static_cast<std::size_t>(count), cudaMemcpyHostToDevice));
+    std::vector<Impl*> all{impl_.get()};
+    for (auto& x : shards_) all.push_back(x.get());
+    const char* in = static_cast<const char*>(src);
+    for (Impl* sh : all) {
+        const auto& Q = sh->pops.at(pop);
+        std::size_t e2;
+        void* d2 = field_ptr(Q.dev, field, e2);
+        if (Q.sharded && field == kFieldFlagged) {
+            // a split population's NaN counter is a sum over shards: the value
+            // goes to shard / rank 0, the others restart from 0
+            const bool first = sh == impl_.get() && (shards_.size() > 0 || m.cfg.rank == 0);
+            const unsigned long long zero = 0;
+            CK(cudaMemcpy(d2, first ? src : &zero, 8, cudaMemcpyHostToDevice));
+            continue;
+        }
+        if (!Q.sharded) {  // whole populations are replicated on every shard
+            CK(cudaMemcpy(d2, in, esz * static_cast<std::size_t>(count), cudaMemcpyHostToDevice));
+            continue;
+        }
+        const std::int64_t k = std::max<std::int64_t>(0, std::min<std::int64_t>(Q.n, count - Q.lo));
+        if (k > 0) CK(cudaMemcpy(d2, in + esz * Q.lo, esz * k, cudaMemcpyHostToDevice));
+    }
 }
+
+void DeviceEngine::shard_range(int pop, int& lo, int& n, int& nGlobal) const {
+    const auto& P = impl_->pops.at(pop);
+    lo = P.sharded ? P.lo : 0;
+    n = P.n;
+    nGlobal = P.nGlobal;
+}
+
+int DeviceEngine::world() const { return impl_->world; }
 
 void DeviceEngine::collect_raster(std::vector<std::int32_t>& counts,
                                   std::vector<std::int32_t>& neurons) {

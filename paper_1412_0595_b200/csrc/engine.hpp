@@ -31,6 +31,9 @@ struct HostPop {
     // RNG stream ("<name>/source" or "<name>/noise"): MT19937-64 state
     std::array<std::uint64_t, 312> mt{};
     int mtPos = 312;
+    // shard of a population split across ranks: neurons [lo, lo + n) of
+    // nGlobal, ranks own chunk neurons each (nGlobal == 0: not split)
+    int nGlobal = 0, lo = 0, chunk = 0;
 };
 
 // One synapse group after gen_fixed_outdegree, gScale and StorageMode.
@@ -69,7 +72,45 @@ struct EngineConfig {
     std::int64_t rasterCapacity = 0;  // 0 = automatic
     bool profile = false;
     bool forceStepMode = false;
+    // multi-GPU: this process is rank `rank` of `world` (NCCL communicator
+    // from commId, one process per GPU).  virtualWorld > 1 instead runs that
+    // many shards inside this engine on one device (exchange by device
+    // copies) -- the same kernels, for testing the sharded path on one GPU.
+    int rank = 0, world = 1, virtualWorld = 0;
+    int shardMinSize = 64;  // CondLif populations at least this large are split
+    bool hasCommId = false;
+    std::array<unsigned char, 128> commId{};
 };
+
+// Which populations a world of R ranks splits, and where (host, no CUDA).
+// bounds[p] is empty for a whole population, else R+1 offsets: rank r owns
+// neurons [bounds[p][r], bounds[p][r+1]).  Split populations are CondLif
+// populations of at least max(minSize, R) neurons; ranges are multiples of
+// 32 neurons (whole spike-bitmask words) for populations of >= 1024*R
+// neurons, of 4 otherwise.  Requires a feed-forward population graph.
+struct ShardPlan {
+    int world = 1;
+    std::vector<std::vector<int>> bounds;
+    std::vector<int> chunk;  // bounds[p][r] = min(r * chunk[p], n)
+    bool split(int p) const { return !bounds[p].empty(); }
+};
+ShardPlan plan_shards(const HostNet& net, int world, int minSize);
+
+// Matrices owned by a rank's local network (column slices).
+struct ShardStore {
+    std::vector<std::vector<float>> f;
+    std::vector<std::vector<std::int32_t>> i32;
+    std::vector<std::vector<std::int64_t>> i64;
+};
+// The local network of one rank: split populations shrink to the rank's
+// range (nGlobal / lo set); a group into a split population keeps the post
+// columns of that range (dense: row-major [nPre][nLocal]; CRS: entries with
+// postInd in range, rebased), rows are untouched -- its pre population's
+// spike list is global after the exchange.
+HostNet shard_net(const HostNet& net, const ShardPlan& plan, int rank, ShardStore& store);
+
+// NCCL unique id for a new communicator (libnccl loaded on first use).
+std::array<unsigned char, 128> comm_unique_id();
 
 struct KernelStat {
     std::string name;
@@ -111,6 +152,12 @@ public:
     void discard_raster();
     void spike_totals(std::vector<std::int64_t>& perPop);
 
+    // Neurons of population pop held by this process: [lo, lo + n) of
+    // nGlobal.  State pull/push of a split population move that local slice
+    // (virtual shards: the whole population); FLAGGED is the global sum.
+    void shard_range(int pop, int& lo, int& n, int& nGlobal) const;
+    int world() const;
+
     void* stream() const;
     int window() const;
     int block_size(int pop) const;
@@ -123,7 +170,9 @@ public:
     struct Impl;
 
 private:
-    std::unique_ptr<Impl> impl_;
+    std::unique_ptr<Impl> impl_;                 // rank / shard 0
+    std::vector<std::unique_ptr<Impl>> shards_;  // virtual shards 1..R-1
+    void lockstep(int W);
 };
 
 // Standalone kernels over caller host arrays (reference propagate /

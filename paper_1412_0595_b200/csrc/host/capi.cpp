@@ -207,7 +207,41 @@ ssb::EngineConfig to_config(const ssb_engine_opts* o) {
     c.rasterCapacity = o->raster_capacity;
     c.profile = o->profile != 0;
     c.forceStepMode = o->force_step_mode != 0;
+    c.rank = o->rank;
+    c.world = std::max(1, static_cast<int>(o->world_size));
+    c.virtualWorld = o->virtual_world;
+    if (o->shard_min_size > 0) c.shardMinSize = o->shard_min_size;
+    c.hasCommId = o->has_comm_id != 0;
+    std::memcpy(c.commId.data(), o->comm_id, 128);
     return c;
+}
+
+// Population kinds, sizes and group endpoints of a spec (no matrices): what
+// the shard plan reads.
+ssb::HostNet skeleton(const NetworkSpec& spec) {
+    ssb::HostNet net;
+    for (const auto& p : spec.populations) {
+        ssb::HostPop hp;
+        hp.name = p.name;
+        hp.n = p.size;
+        hp.kind = p.model == ModelKind::CondLif ? ssb::kCondLif
+                  : p.model == ModelKind::PoissonSource ? ssb::kPoisson
+                                                         : ssb::kIzhikevich;
+        net.pops.push_back(hp);
+    }
+    auto index = [&](const std::string& n) {
+        for (std::size_t i = 0; i < spec.populations.size(); ++i)
+            if (spec.populations[i].name == n) return static_cast<int>(i);
+        throw SpecError("unknown population '" + n + "'");
+    };
+    for (const auto& g : spec.synapses) {
+        ssb::HostGroup hg;
+        hg.name = g.name;
+        hg.pre = index(g.pre);
+        hg.post = index(g.post);
+        net.groups.push_back(hg);
+    }
+    return net;
 }
 
 StorageMode to_mode(int m) {
@@ -372,6 +406,8 @@ void ssb_engine_default_opts(ssb_engine_opts* o) {
     o->window = c.window;
     o->use_graphs = 1;
     o->heavy_pre_threshold = c.heavyPreThreshold;
+    o->world_size = 1;
+    o->shard_min_size = c.shardMinSize;
 }
 
 uint64_t ssb_fnv1a64(const char* label) { return fnv1a64(str(label)); }
@@ -431,6 +467,74 @@ int ssb_build_group(const ssb_net_desc* net, int32_t storage_mode, int32_t group
                 std::memcpy(row_start, s->rowStart.data(), s->rowStart.size() * sizeof(int64_t));
             }
         }
+    });
+}
+
+int ssb_shard_plan(const ssb_net_desc* net, int32_t world, int32_t min_size, int64_t* bounds,
+                   char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const NetworkSpec spec = to_spec(net);
+        require_valid(spec);
+        if (world < 1) throw SpecError("world must be >= 1");
+        const ssb::ShardPlan plan =
+            ssb::plan_shards(skeleton(spec), world, min_size > 0 ? min_size : 64);
+        for (std::size_t p = 0; p < spec.populations.size(); ++p)
+            for (int r = 0; r <= world; ++r)
+                bounds[p * (world + 1) + r] = plan.split(static_cast<int>(p)) ? plan.bounds[p][r] : -1;
+    });
+}
+
+int ssb_shard_group(const ssb_net_desc* net, int32_t storage_mode, int32_t group, int32_t world,
+                    int32_t rank, int32_t min_size, int32_t* storage, int32_t* n_pre,
+                    int32_t* n_post, int64_t* nnz, float* values, int32_t* post_ind,
+                    int64_t* row_start, int64_t cap, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const NetworkSpec spec = to_spec(net);
+        require_valid(spec);
+        if (group < 0 || group >= static_cast<int32_t>(spec.synapses.size()))
+            throw SpecError("group index out of range");
+        if (world < 1) throw SpecError("world must be >= 1");
+        ssb::HostNet skel = skeleton(spec);
+        const ssb::ShardPlan plan = ssb::plan_shards(skel, world, min_size > 0 ? min_size : 64);
+        std::optional<DenseMatrix> d;
+        std::optional<CrsMatrix> s;
+        ssb::build_group_matrix(spec, to_mode(storage_mode), group, d, s);
+        auto& g = skel.groups[group];
+        g.dense = d.has_value();
+        g.nPre = d ? d->nPre : s->nPre;
+        g.nPost = d ? d->nPost : s->nPost;
+        g.preCount = g.nPre;
+        if (d) {
+            g.W = d->weights.data();
+        } else {
+            g.g = s->gValues.data();
+            g.ind = s->postInd.data();
+            g.rowStart = s->rowStart.data();
+            g.nnz = s->nnz();
+        }
+        ssb::ShardStore store;
+        const ssb::HostNet local = ssb::shard_net(skel, plan, rank, store);
+        const auto& L = local.groups[group];
+        *storage = L.dense ? SSB_STORAGE_DENSE : SSB_STORAGE_SPARSE;
+        *n_pre = L.nPre;
+        *n_post = L.nPost;
+        *nnz = L.dense ? static_cast<int64_t>(L.nPre) * L.nPost : L.nnz;
+        if (!values) return;
+        if (cap < *nnz) throw SpecError("buffer too small");
+        if (L.dense) {
+            std::memcpy(values, L.W, static_cast<std::size_t>(*nnz) * sizeof(float));
+        } else {
+            std::memcpy(values, L.g, static_cast<std::size_t>(*nnz) * sizeof(float));
+            std::memcpy(post_ind, L.ind, static_cast<std::size_t>(*nnz) * sizeof(int32_t));
+            std::memcpy(row_start, L.rowStart, (static_cast<std::size_t>(L.nPre) + 1) * sizeof(int64_t));
+        }
+    });
+}
+
+int ssb_comm_unique_id(uint8_t* out128, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const auto id = ssb::comm_unique_id();
+        std::memcpy(out128, id.data(), 128);
     });
 }
 
@@ -524,6 +628,21 @@ int ssb_step(ssb_sim* sim, int64_t n) {
 }
 
 int64_t ssb_steps_total(const ssb_sim* sim) { return sim ? sim->core->steps_total() : -1; }
+
+int32_t ssb_world(const ssb_sim* sim) { return sim ? sim->core->engine().world() : 0; }
+
+int ssb_shard_range(const ssb_sim* sim, int32_t pop, int64_t* lo, int64_t* n_local,
+                    int64_t* n_global) {
+    if (!sim) return SSB_ERR_SPEC;
+    return on_sim(const_cast<ssb_sim*>(sim), [&](ssb::SimCore& c) {
+        if (pop < 0 || pop >= c.n_pops()) throw SpecError("population index out of range");
+        int l, n, g;
+        c.engine().shard_range(pop, l, n, g);
+        *lo = l;
+        *n_local = n;
+        *n_global = g;
+    });
+}
 int64_t ssb_steps_done(const ssb_sim* sim) { return sim ? sim->core->steps_done() : -1; }
 
 int ssb_sync(ssb_sim* sim) {

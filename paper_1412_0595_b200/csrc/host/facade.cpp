@@ -20,6 +20,12 @@ ssb::EngineConfig to_config(const EngineOptions& o) {
     c.rasterCapacity = o.rasterCapacity;
     c.profile = o.profile;
     c.forceStepMode = o.forceStepMode;
+    c.rank = o.rank;
+    c.world = std::max(1, o.world);
+    c.virtualWorld = o.virtualWorld;
+    if (o.shardMinSize > 0) c.shardMinSize = o.shardMinSize;
+    c.hasCommId = o.hasCommId;
+    c.commId = o.commId;
     return c;
 }
 
@@ -246,4 +252,8 @@ double avg_spike(const Raster& raster, const std::string& population, double dur
     return static_cast<double>(count) / (static_cast<double>(size) * (durationMs / 1000.0));
 }
 
+}  // namespace synscale
+
+namespace synscale {
+std::array<unsigned char, 128> comm_unique_id() { return ssb::comm_unique_id(); }
 }  // namespace synscale

@@ -360,6 +360,14 @@ class EngineOptions:
     rasterCapacity: int = 0
     profile: bool = False
     forceStepMode: bool = False
+    # multi-GPU: one process per GPU, rank of world, NCCL id
+    # from comm_unique_id() on rank 0 (broadcast by the caller); virtualWorld > 1
+    # runs that many shards in this process on one GPU (tests the split path)
+    rank: int = 0
+    world: int = 1
+    virtualWorld: int = 0
+    shardMinSize: int = 0
+    commId: Optional[bytes] = None
 
     def to_c(self) -> L.ssb_engine_opts:
         o = L.ssb_engine_opts()
@@ -375,6 +383,16 @@ class EngineOptions:
         o.raster_capacity = self.rasterCapacity
         o.profile = int(self.profile)
         o.force_step_mode = int(self.forceStepMode)
+        o.rank = self.rank
+        o.world_size = max(1, self.world)
+        o.virtual_world = self.virtualWorld
+        if self.shardMinSize:
+            o.shard_min_size = self.shardMinSize
+        if self.commId is not None:
+            if len(self.commId) != 128:
+                raise ValueError("commId must be 128 bytes (comm_unique_id())")
+            o.has_comm_id = 1
+            C.memmove(o.comm_id, bytes(self.commId), 128)
         return o
 
 
@@ -455,6 +473,17 @@ class Simulation:
 
     def steps_total(self) -> int:
         return int(lib.ssb_steps_total(self._h))
+
+    def world(self) -> int:
+        """Ranks (or virtual shards) the network is split over (1: whole)."""
+        return int(lib.ssb_world(self._h))
+
+    def shard_range(self, pop: Union[int, str]) -> Tuple[int, int, int]:
+        """(lo, n_local, n_global): this process's neurons of population pop."""
+        pi = pop if isinstance(pop, int) else self.spec.pop_index(pop)
+        lo, nl, ng = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(lib.ssb_shard_range(self._h, pi, C.byref(lo), C.byref(nl), C.byref(ng)))
+        return lo.value, nl.value, ng.value
 
     def steps_done(self) -> int:
         return int(lib.ssb_steps_done(self._h))
@@ -720,6 +749,52 @@ def build_group(spec: NetworkSpec, group: Union[int, str],
                                C.byref(npost), C.byref(nnz), _fptr(vals), _iptr(ind), _lptr(rs),
                                vals.size, err, len(err)), err.value.decode())
     return "sparse", (vals, ind, rs)
+
+
+def shard_plan(spec: NetworkSpec, world: int, minSize: int = 0) -> Dict[str, Optional[List[int]]]:
+    """Neuron ranges of a world of `world` ranks per population (None: whole,
+    replicated on every rank), as the engine splits it (host, no GPU)."""
+    desc = NetDesc(spec)
+    npop = len(spec.populations)
+    b = np.empty(npop * (world + 1), np.int64)
+    err = _err()
+    _raise(lib.ssb_shard_plan(desc.ptr, world, minSize, _lptr(b), err, len(err)),
+           err.value.decode())
+    b = b.reshape(npop, world + 1)
+    return {p.name: (None if b[i, 0] < 0 else [int(x) for x in b[i]])
+            for i, p in enumerate(spec.populations)}
+
+
+def shard_group(spec: NetworkSpec, group: Union[int, str], world: int, rank: int,
+                mode: StorageMode = StorageMode.FromSpec, minSize: int = 0):
+    """Group connectivity as rank `rank` of `world` holds it (column slice of a
+    split post population); same return shape as build_group."""
+    gi = group if isinstance(group, int) else spec.group_index(group)
+    desc = NetDesc(spec)
+    st, npre, npost, nnz = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
+    err = _err()
+    args = (desc.ptr, int(mode), gi, world, rank, minSize, C.byref(st), C.byref(npre),
+            C.byref(npost), C.byref(nnz))
+    _raise(lib.ssb_shard_group(*args, None, None, None, 0, err, len(err)), err.value.decode())
+    vals = np.empty(nnz.value, np.float32)
+    if st.value == L.STORAGE_DENSE:
+        _raise(lib.ssb_shard_group(*args, _fptr(vals), None, None, vals.size, err, len(err)),
+               err.value.decode())
+        return "dense", vals.reshape(npre.value, npost.value)
+    ind = np.empty(nnz.value, np.int32)
+    rs = np.empty(npre.value + 1, np.int64)
+    _raise(lib.ssb_shard_group(*args, _fptr(vals), _iptr(ind), _lptr(rs), vals.size, err,
+                               len(err)), err.value.decode())
+    return "sparse", (vals, ind, rs)
+
+
+def comm_unique_id() -> bytes:
+    """NCCL unique id for EngineOptions.commId (rank 0 creates, the caller
+    broadcasts it, e.g. with torch.distributed.broadcast_object_list)."""
+    out = (C.c_uint8 * 128)()
+    err = _err()
+    _raise(lib.ssb_comm_unique_id(out, err, len(err)), err.value.decode())
+    return bytes(out)
 
 
 def mem_sparse_elements(nnz: int, nPost: int) -> int:

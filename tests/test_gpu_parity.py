@@ -332,3 +332,68 @@ def test_block_policies_do_not_change_results():
         key = (r.raster.neuron.tobytes(), sim.pull(2, "v").tobytes())
         ref = ref or key
         assert key == ref, kw
+
+
+# ---- split populations (multi-GPU decomposition) --------------
+# virtualWorld = R runs the R shards of a world inside one process on this
+# GPU: the same kernels and the same per-window exchange (local bitmasks
+# gathered in rank order, assembled, compacted) with device copies in place
+# of the NCCL all-gather.  Results must equal the unsplit engine bit for bit.
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("name", ["cfg2_100ms", "cfg3_20ms", "cfg2_fromspec_100ms"])
+def test_split_world_matches_reference_golden(golden, name, world):
+    spec, mode = GOLDEN[name]()
+    g = golden["runs"][name]
+    sim = gpu_sim(spec, mode, window=64, virtualWorld=world)
+    assert sim.world() == world
+    lo, nl, ng = sim.shard_range("kc")
+    assert (lo, ng) == (0, spec.populations[spec.pop_index("kc")].size) and nl < ng
+    r = sim.finish()
+    assert len(r.raster) == g["n_events"]
+    assert specs.sha(r.raster.step, r.raster.population, r.raster.neuron) == g["raster_sha"]
+    assert [r.avgSpike[p.name] for p in spec.populations] == g["rates"]
+    assert r.sumNaNs == g["sum_nans"]
+    for pi, p in enumerate(spec.populations):
+        for f, h in g["state_sha"][p.name].items():
+            if p.model == S.ModelKind.PoissonSource and f in ("v", "gExc", "gInh"):
+                continue
+            assert specs.sha(sim.pull(pi, f)) == h, (p.name, f)
+
+
+@pytest.mark.parametrize("window", [1, 5])
+def test_split_world_stepwise_state_and_fault_injection(oracle_mod, window):
+    """Small windows, state pulled (gathered across shards) every few steps,
+    and a NaN injected through push (scattered to its shard)."""
+    spec, mode = specs.config_spec(2, 12.0)
+    g = gpu_sim(spec, mode, window=window, virtualWorld=2, shardMinSize=32)
+    o = cpu_sim(oracle_mod, spec, mode)
+    kc = spec.pop_index("kc")
+    for t in range(0, 120, 15):
+        g.step(15)
+        o.step(15)
+        assert_state_equal(g, o, spec, f"t={t + 15}")
+        if t == 45:
+            v = o.state(kc, "v")
+            v[7000] = np.nan  # lives on shard 1
+            g.push(kc, "v", v)
+            o.set_state(kc, "v", v)
+    rg, ro = g.finish(), o.finish()
+    assert rg.sumNaNs == o.sum_nans() >= 1
+    assert np.array_equal(rg.raster.step, ro[0])
+    assert np.array_equal(rg.raster.population, ro[1])
+    assert np.array_equal(rg.raster.neuron, ro[2])
+
+
+def test_concurrent_simulations_of_different_sizes(golden):
+    """Two live engines with different shared-memory plans (the per-kernel
+    dynamic shared-memory limit is process-wide; a smaller engine built
+    later must not lower it under the larger one)."""
+    spec3, mode3 = GOLDEN["cfg3_20ms"]()
+    spec1, mode1 = GOLDEN["cfg1_1000ms"]()
+    big = gpu_sim(spec3, mode3)
+    small = gpu_sim(spec1, mode1)
+    for sim, name in ((big, "cfg3_20ms"), (small, "cfg1_1000ms")):
+        r = sim.finish()
+        assert specs.sha(r.raster.step, r.raster.population, r.raster.neuron) == \
+            golden["runs"][name]["raster_sha"]
