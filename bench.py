@@ -13,10 +13,14 @@ buffers: spec -> ssb_create (connectivity generated on the host, uploaded)
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N > 1 (torchrun): weak scaling over independent network replicas, one per
-GPU (the reference's own parallelism model, calibration.cpp:76-84): each rank
-simulates its own config-3 network with a rank-dependent seed; value is the
-sum over ranks of events / (max over ranks of time).
+N > 1 (torchrun), default --scaling split: weak scaling of ONE network split
+over the N GPUs: N x 100,000 KC (gScales per SURVEY.md §8(d):
+kc_dn = 30 / nKC), KC and DN split by neuron ranges, PN / LHI replicated, each
+window's KC / DN spike bitmasks all-gathered over NCCL; value = the network's
+synaptic events / (max over ranks of device time).  At N = 1 this is config 3
+exactly.  --scaling replicas runs independent config-3 networks instead (the
+reference's own parallelism, calibration.cpp:76-84), and is the fallback when
+the split run cannot start.
 """
 from __future__ import annotations
 
@@ -51,6 +55,19 @@ def workload_config(window=None):
     if window is not None:
         cfg["window_steps"] = window
     return cfg
+
+
+def scaling_config(mode, world, fallback=None):
+    if mode == "split":
+        return {"parallelism": f"split{world}", "n_kc_total": N_KC * world,
+                "split": "KC and DN by neuron ranges, PN/LHI replicated, per-window NCCL "
+                         "all-gather of spike bitmasks"}
+    if mode == "replicas":
+        cfg = {"parallelism": f"replicas{world}", "replicas": world}
+        if fallback:
+            cfg["split_failed"] = fallback
+        return cfg
+    return {"parallelism": "single"}
 
 
 def make_spec(seconds: float, seed: int = 7):
@@ -251,6 +268,7 @@ def main():
     ap.add_argument("--window", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scaling", default="split", choices=["split", "replicas"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -273,14 +291,48 @@ def main():
     torch.cuda.set_device(dev)
 
     total_s = args.warmup + args.steps + 1
-    spec = make_spec(total_s, seed=7 + rank)
+    mode = args.scaling if world > 1 else "single"
+    fallback = None
+
+    def start(mode):
+        """(spec, sim) of this rank; the split mode builds the same N x 100k
+        network on every rank and the engine keeps this rank's part."""
+        import specs
+        if mode == "split":
+            spec = specs.mbody_spec(N_KC * world, FRAC, total_s * 1000.0, seed=7)
+            cid = [S.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(cid, src=0)
+            opts = S.EngineOptions(device=dev, window=args.window, world=world, rank=rank,
+                                   commId=cid[0])
+        else:
+            spec = make_spec(total_s, seed=7 + rank)
+            opts = S.EngineOptions(device=dev, window=args.window)
+        sim = S.Simulation(spec, S.StorageMode.FromSpec, opts)
+        sim.step(STEPS_PER_SIM_SECOND)  # first warm-up step
+        sim.sync()
+        return spec, sim
+
     t0 = time.perf_counter()
-    sim = S.Simulation(spec, S.StorageMode.FromSpec, S.EngineOptions(device=dev, window=args.window))
+    if mode == "split":
+        err, spec, sim = "", None, None
+        try:
+            spec, sim = start("split")
+        except Exception as exc:  # noqa: BLE001 -- reported in the JSON line
+            err = f"{type(exc).__name__}: {exc}"
+        bad = torch.tensor([1.0 if err else 0.0], device=f"cuda:{dev}")
+        dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        if bad.item() > 0:
+            if sim is not None:
+                sim.close()
+            fallback = err or "another rank failed"
+            mode = "replicas"
+    if mode != "split":
+        spec, sim = start(mode)
     build_s = time.perf_counter() - t0
     stream = torch.cuda.ExternalStream(sim.stream(), device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{dev}")
 
-    for _ in range(args.warmup):
+    for _ in range(args.warmup - 1):
         sim.step(STEPS_PER_SIM_SECOND)
     sim.sync()
 
@@ -315,7 +367,8 @@ def main():
         tt = torch.tensor([t_local], device=f"cuda:{dev}", dtype=torch.float64)
         ee = torch.tensor([ev_local], device=f"cuda:{dev}", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dist.all_reduce(ee, op=dist.ReduceOp.SUM)
+        if mode == "replicas":  # independent networks: add them up
+            dist.all_reduce(ee, op=dist.ReduceOp.SUM)
         t_max, ev_sum = float(tt.item()), float(ee.item())
     value = ev_sum / t_max
     sim_seconds = args.steps
@@ -385,7 +438,7 @@ def main():
                 "kernels": rf["kernels"]}
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         try:
             from oracle import oracle as O
             if O.have_ref():
@@ -405,7 +458,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded build_mbody_net, reference RNG streams)",
             "config": dict(workload_config(args.window), l2="flushed (256 MiB write) between steps",
-                           replicas=world),
+                           **scaling_config(mode, world, fallback)),
             "sim_wall": sim_seconds / t_max,
             "us_per_timestep": t_max / (sim_seconds * STEPS_PER_SIM_SECOND) * 1e6,
             "build_s": build_s,

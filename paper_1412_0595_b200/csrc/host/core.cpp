@@ -3,7 +3,11 @@
 // result collection.
 #include "core.hpp"
 
+#include <atomic>
 #include <cmath>
+#include <exception>
+#include <numeric>
+#include <thread>
 
 #include "connect_detail.hpp"
 
@@ -53,6 +57,16 @@ void build_group_matrix(const NetworkSpec& spec, StorageMode mode, int gi,
         DenseMatrix m;
         m.nPre = nPre;
         m.nPost = nPost;
+        if (rows.full && gs.baseWeight.kind == WeightDist::Kind::Constant) {
+            // all-to-all with one constant weight (lhi_kc, kc_dn, pn_lhi): every
+            // entry is the same scaled value and no stream is drawn
+            // (matrix.cpp:128-139 draws nothing for a constant distribution)
+            scalar w = scalar(0);
+            if (nPre > 0 && rows.next()) w = scaled(rows.vals[0]);
+            m.weights.assign(static_cast<std::size_t>(nPre) * static_cast<std::size_t>(nPost), w);
+            dense = std::move(m);
+            return;
+        }
         m.weights.assign(static_cast<std::size_t>(nPre) * static_cast<std::size_t>(nPost), scalar(0));
         for (std::int32_t r = 0; rows.next(); ++r) {
             scalar* dst = m.weights.data() + static_cast<std::size_t>(r) * nPost;
@@ -137,6 +151,41 @@ SimCore::SimCore(const NetworkSpec& spec, StorageMode mode, const EngineConfig& 
 
     dense_.resize(spec_.synapses.size());
     sparse_.resize(spec_.synapses.size());
+    {
+        // groups are independent (own derived seeds and streams): build them
+        // on host threads, largest first
+        const std::size_t ng = spec_.synapses.size();
+        std::vector<std::size_t> todo(ng);
+        std::iota(todo.begin(), todo.end(), 0);
+        auto work = [&](std::size_t gi) {
+            const auto& gs = spec_.synapses[gi];
+            const auto* post = spec_.find_population(gs.post);
+            return static_cast<double>(gs.outDegree) *
+                   (spec_.find_population(gs.pre) ? spec_.find_population(gs.pre)->size : 0) +
+                   (post ? post->size : 0);
+        };
+        std::sort(todo.begin(), todo.end(), [&](auto a, auto b) { return work(a) > work(b); });
+        std::atomic<std::size_t> next{0};
+        std::vector<std::exception_ptr> errs(ng);
+        auto run = [&] {
+            for (std::size_t i; (i = next.fetch_add(1)) < ng;) {
+                try {
+                    build_group_matrix(spec_, mode_, static_cast<int>(todo[i]), dense_[todo[i]],
+                                       sparse_[todo[i]]);
+                } catch (...) {
+                    errs[todo[i]] = std::current_exception();
+                }
+            }
+        };
+        const unsigned nt = static_cast<unsigned>(std::min<std::size_t>(
+            ng, std::max(1u, std::min(8u, std::thread::hardware_concurrency()))));
+        std::vector<std::thread> pool;
+        for (unsigned t = 1; t < nt; ++t) pool.emplace_back(run);
+        run();
+        for (auto& t : pool) t.join();
+        for (auto& e : errs)  // the first failing group in spec order, as sequentially
+            if (e) std::rethrow_exception(e);
+    }
     for (std::size_t gi = 0; gi < spec_.synapses.size(); ++gi) {
         const auto& gs = spec_.synapses[gi];
         HostGroup g;
@@ -149,7 +198,6 @@ SimCore::SimCore(const NetworkSpec& spec, StorageMode mode, const EngineConfig& 
         g.nPre = g.preCount;
         g.nPost = spec_.populations[g.post].size;
         g.outDegree = gs.outDegree;
-        build_group_matrix(spec_, mode_, static_cast<int>(gi), dense_[gi], sparse_[gi]);
         g.dense = dense_[gi].has_value();
         if (g.dense) {
             g.W = dense_[gi]->weights.data();
