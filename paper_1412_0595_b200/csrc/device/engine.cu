@@ -388,8 +388,10 @@ struct DeviceEngine::Impl {
 int DeviceEngine::Impl::choose_block(int n, const std::function<std::int64_t(int)>& smemFor,
                                      const void* kernelFn) const {
     const int single = std::min(1024, round_up(std::max(n, 1), 32));
-    if (cfg.blockSize > 0) return std::min(round_up(cfg.blockSize, 32), 1024);
     if (n <= 256) return single;  // one block; extra threads serve the parallel phases
+    // a forced block size applies to the multi-block populations (the ones
+    // whose update the occupancy model sizes)
+    if (cfg.blockSize > 0) return std::min(round_up(cfg.blockSize, 32), 1024);
     int regs = 32, shared = 0, maxThreads = 1024;
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, kernelFn) == cudaSuccess) {
@@ -727,6 +729,9 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             G.nTiles = (g.nPost + G.segTile - 1) / G.segTile;
             G.g = upload<float>(g.g, static_cast<std::size_t>(g.nnz));
             G.ind = upload<int>(g.ind, static_cast<std::size_t>(g.nnz));
+            // every row holds every post (all-to-all stored sparse): the values
+            // are the dense row-major matrix, entry for entry
+            G.fullRows = g.nnz == static_cast<std::int64_t>(g.preCount) * g.nPost ? 1 : 0;
             long long* rs = upload<long long>(
                 reinterpret_cast<const long long*>(g.rowStart), static_cast<std::size_t>(g.nPre) + 1);
             int* seg = alloc<int>(static_cast<std::size_t>(g.preCount) * (G.nTiles + 1));
@@ -836,7 +841,6 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     allow(reinterpret_cast<const void*>(&ssbk::condlif_window_kernel), std::max(maxSmem, 4096));
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_warp_kernel), kWarpRingBytes);
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_pipe_kernel), ring_smem());
-    allow(reinterpret_cast<const void*>(&ssbk::sparse_window_kernel), 4096 * 4);
     if (const char* e = std::getenv("SSB_DENSE_KERNEL")) usePipe = std::string(e) == "pipe";
     CK(cudaStreamSynchronize(stream));
 }
@@ -862,12 +866,14 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t s) {
                 const auto& G = A.g[k];
                 const int gi = P.accGroups[a][k];
                 float* out = A.buf + P.n;  // row w = 1
-                if (G.dense) {
-                    launch_dense(G, groupMeta[gi].name, "dense_window:", out, P.n, 1, W, k == 0, s);
+                if (G.dense || G.fullRows) {
+                    ssbk::GroupDev D = G;
+                    if (!G.dense) D.W = G.g;  // full CRS rows = dense rows
+                    launch_dense(D, groupMeta[gi].name, "dense_window:", out, P.n, 1, W, k == 0, s);
                 } else {
                     dim3 grid(G.nTiles, W);
                     launch("sparse_window:" + groupMeta[gi].name, [&] {
-                        ssbk::sparse_window_kernel<<<grid, G.segTile, G.segTile * 4, s>>>(
+                        ssbk::sparse_window_kernel<<<grid, G.segTile, 0, s>>>(
                             G, out, P.n, 1, k == 0);
                     });
                 }
@@ -930,7 +936,7 @@ void DeviceEngine::Impl::enqueue_tail(int W, int b, cudaStream_t s) {
                 } else {
                     dim3 grid(G.nTiles, 1);
                     launch("sparse_deliver:" + groupMeta[gi].name, [&] {
-                        ssbk::sparse_window_kernel<<<grid, G.segTile, G.segTile * 4, s>>>(G, out, 0,
+                        ssbk::sparse_window_kernel<<<grid, G.segTile, 0, s>>>(G, out, 0,
                                                                                          W, k == 0);
                     });
                 }

@@ -64,10 +64,7 @@ void device_propagate_crs_dev(const float* g, const std::int32_t* ind, const std
     (void)nPre;
     if (nPost <= 0 || nSpikes <= 0) return;
     const int nTiles = (nPost + tile - 1) / tile;
-    if (tile * 4 > 48 * 1024)
-        CK(cudaFuncSetAttribute(ssbk::propagate_crs_kernel,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, tile * 4));
-    ssbk::propagate_crs_kernel<<<nTiles, tile, tile * 4, static_cast<cudaStream_t>(stream)>>>(
+    ssbk::propagate_crs_kernel<<<nTiles, tile, 0, static_cast<cudaStream_t>(stream)>>>(
         g, ind, seg, nTiles, nPost, spikes, nSpikes, acc);
     CK(cudaGetLastError());
 }
