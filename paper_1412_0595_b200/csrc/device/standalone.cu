@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <memory>
 #include <string>
 #include <vector>
@@ -41,9 +42,16 @@ void device_propagate_dense_dev(const float* w, int nPre, int nPost, const std::
                                 int nSpikes, float* acc, void* stream) {
     (void)nPre;
     if (nPost <= 0 || nSpikes <= 0) return;
-    ssbk::propagate_dense_kernel<<<(nPost + 127) / 128, 128, 0,
-                                   static_cast<cudaStream_t>(stream)>>>(w, nPost, spikes, nSpikes,
-                                                                        acc);
+    const bool vec = nPost % 4 == 0 && reinterpret_cast<std::uintptr_t>(w) % 16 == 0 &&
+                     reinterpret_cast<std::uintptr_t>(acc) % 16 == 0;
+    if (vec)
+        ssbk::propagate_dense4_kernel<<<(nPost / 4 + 255) / 256, 256, 0,
+                                        static_cast<cudaStream_t>(stream)>>>(w, nPost, spikes,
+                                                                             nSpikes, acc);
+    else
+        ssbk::propagate_dense_kernel<<<(nPost + 127) / 128, 128, 0,
+                                       static_cast<cudaStream_t>(stream)>>>(w, nPost, spikes,
+                                                                            nSpikes, acc);
     CK(cudaGetLastError());
 }
 

@@ -50,19 +50,20 @@ def launches(path):
 def launch_table(per, title):
     agg = collections.OrderedDict()
     for d in per.values():
-        a = agg.setdefault(d["name"], {"n": 0, "us": 0.0, "rd": 0.0, "wr": 0.0})
+        grid = d["grid"].strip("()").replace(", 1, 1", "").replace(" ", "")
+        a = agg.setdefault(f"{d['name']} [{grid}]", {"n": 0, "us": 0.0, "rd": 0.0, "wr": 0.0})
         a["n"] += 1
         a["us"] += d.get("gpu__time_duration.sum", 0.0)
         a["rd"] += d.get("dram__bytes_read.sum", 0.0)
         a["wr"] += d.get("dram__bytes_write.sum", 0.0)
     tot = sum(a["us"] for a in agg.values()) or 1.0
-    lines = [title, "", f"{'kernel':28s} {'launches':>8s} {'total us':>11s} {'mean us':>9s} "
+    lines = [title, "", f"{'kernel (grid)':40s} {'launches':>8s} {'total us':>11s} {'mean us':>9s} "
              f"{'share':>6s} {'DRAM rd MB/launch':>18s} {'DRAM wr MB/launch':>18s}"]
     for k, a in sorted(agg.items(), key=lambda kv: -kv[1]["us"]):
-        lines.append(f"{k:28s} {a['n']:8d} {a['us']:11.1f} {a['us'] / a['n']:9.2f} "
+        lines.append(f"{k:40s} {a['n']:8d} {a['us']:11.1f} {a['us'] / a['n']:9.2f} "
                      f"{a['us'] / tot * 100:5.1f}% {a['rd'] / a['n'] / 1e6:18.3f} "
                      f"{a['wr'] / a['n'] / 1e6:18.3f}")
-    lines.append(f"{'total':28s} {sum(a['n'] for a in agg.values()):8d} {tot:11.1f}")
+    lines.append(f"{'total':40s} {sum(a['n'] for a in agg.values()):8d} {tot:11.1f}")
     return "\n".join(lines) + "\n"
 
 

@@ -47,8 +47,11 @@ def density():
             fn()
         ts = []
         for _ in range(reps):
-            flush.zero_()  # inputs cold in L2 (> 126 MB written)
             prep()
+            # inputs cold in L2: read 256 MB (a read leaves clean lines, a
+            # write-flush would make the timed kernel pay for write-backs);
+            # it also keeps the GPU busy while the host enqueues the launch
+            flush.sum(dtype=torch.float32)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             fn()
