@@ -380,10 +380,35 @@ def main():
             dist.destroy_process_group()
         return
 
-    # -- e2e through the public C ABI with host buffers (rank 0, 1 s per step)
+    # -- e2e through the public C ABI with host buffers (rank 0, 1 s per step).
+    # Same scope as the reference arm (which times Simulation::step, not the
+    # constructor): per step, ssb_step(10,000) and the step's raster moved into
+    # host memory (ssb_raster_drain); wall clock.  The network is uploaded once
+    # at construction (like the reference, untimed) and the Poisson drive is
+    # the model's own RNG stream advanced on the device (part of the step), so
+    # no per-step host input exists: h2d_bytes_per_step = 0.  For reference,
+    # e2e.with_build adds construction (host connectivity build + upload) and
+    # ssb_finish of a fresh 1 s run.
     e2e = None
     if not args.no_e2e:
-        e2e_vals, h2d, d2h = [], 0, 0
+        k_e2e = 3
+        spec_e = make_spec(k_e2e + 1.0, seed=11)
+        sim_e = S.Simulation(spec_e, S.StorageMode.FromSpec,
+                             S.EngineOptions(device=dev, window=args.window))
+        sim_e.step(STEPS_PER_SIM_SECOND)
+        held = sim_e.drain_raster()
+        vals, d2h = [], []
+        for _ in range(k_e2e):
+            c0 = sim_e.spike_counts()
+            t0 = time.perf_counter()
+            sim_e.step(STEPS_PER_SIM_SECOND)
+            n = sim_e.drain_raster()
+            t1 = time.perf_counter()
+            vals.append(synaptic_events(spec_e, sim_e.spike_counts() - c0) / (t1 - t0))
+            d2h.append(4 * (n - held))
+            held = n
+        sim_e.close()
+        wb = []
         for i in range(2):
             spec1 = make_spec(1.0, seed=11 + i)
             torch.cuda.synchronize()
@@ -394,24 +419,15 @@ def main():
             t1 = time.perf_counter()
             counts = np.array([np.count_nonzero(r.raster.population == k)
                                for k in range(len(spec1.populations))])
-            e2e_vals.append(synaptic_events(spec1, counts) / (t1 - t0))
-            # bytes actually copied: connectivity + state + RNG state up, raster down
-            nbytes_up = 0
-            for gi, g in enumerate(spec1.synapses):
-                m = sim1.group_dense(g.name)
-                if m is not None:
-                    nbytes_up += m.nbytes
-                else:
-                    gv, ind, rs = sim1.group_sparse(g.name)
-                    nbytes_up += gv.nbytes + ind.nbytes + rs.nbytes
-            nbytes_up += sum(p.size * 4 for p in spec1.populations) + 312 * 8 + 4
-            h2d = nbytes_up
-            d2h = 4 * len(r.raster) + 4 * STEPS_PER_SIM_SECOND * len(spec1.populations)
+            wb.append(synaptic_events(spec1, counts) / (t1 - t0))
             sim1.close()
-        e2e = {"value": max(e2e_vals), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h),
-               "what": "ssb_create (host connectivity build + upload) + 10,000 steps + "
-                       "ssb_finish (raster to host), wall clock, best of 2"}
+        e2e = {"value": statistics.median(vals), "unit": UNIT, "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": int(statistics.median(d2h)),
+               "what": "per bench step: ssb_step(10,000) + ssb_raster_drain (the step's raster "
+                       "events into host memory), wall clock, median of 3; network uploaded "
+                       "once at construction (untimed, as in the reference arm)",
+               "with_build": {"value": max(wb), "what": "ssb_create (host build + upload) + "
+                              "10,000 steps + ssb_finish, wall clock, best of 2"}}
 
     # -- roofline of the dominant kernel (profiled pass)
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")

@@ -318,6 +318,10 @@ SSB_API int ssb_spike_counts(ssb_sim* sim, int64_t* counts, int32_t n_pops);
 /* Drops every recorded event (counts and ids) held so far; bench helper for
  * long runs whose raster is not wanted. */
 SSB_API int ssb_raster_discard(ssb_sim* sim);
+/* Waits for the steps issued so far and moves every event recorded so far into
+ * host memory (the engine otherwise drains in the background); returns the
+ * number of events held on the host in *n_events. */
+SSB_API int ssb_raster_drain(ssb_sim* sim, int64_t* n_events);
 
 /* ---- introspection / measurement ------------------------------------------- */
 SSB_API void* ssb_stream(ssb_sim* sim); /* the handle's cudaStream_t */

@@ -1,6 +1,7 @@
 // engine.cu — DeviceEngine: device memory layout, launch schedule, CUDA
 // graphs and raster management of the windowed step engine.
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <cmath>
@@ -29,6 +30,44 @@ void check(cudaError_t e, const char* what) {
 #define CK(x) check((x), #x)
 
 int round_up(int v, int u) { return (v + u - 1) / u * u; }
+
+// Host store of drained raster events: anonymous mappings with transparent
+// huge pages (first touch of tens of MB in 4 KB pages costs more than the
+// device-to-host copy itself).
+std::shared_ptr<std::int32_t> host_events(std::size_t n) {
+    const std::size_t huge = std::size_t(2) << 20;
+    const std::size_t bytes = (std::max<std::size_t>(n, 1) * 4 + huge - 1) / huge * huge;
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) {
+        return std::shared_ptr<std::int32_t>(new std::int32_t[std::max<std::size_t>(n, 1)],
+                                             std::default_delete<std::int32_t[]>());
+    }
+    madvise(p, bytes, MADV_HUGEPAGE);
+    return std::shared_ptr<std::int32_t>(static_cast<std::int32_t*>(p),
+                                         [bytes](std::int32_t* q) { munmap(q, bytes); });
+}
+
+// memcpy split over a few host threads (pinned staging -> the host store).
+void parallel_copy(void* dst, const void* src, std::size_t bytes) {
+    constexpr std::size_t kMin = std::size_t(2) << 20;
+    const unsigned nt = static_cast<unsigned>(std::min<std::size_t>(4, bytes / kMin));
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    const std::size_t part = (bytes / nt + 63) / 64 * 64;
+    std::vector<std::thread> ts;
+    for (unsigned t = 1; t < nt; ++t) {
+        const std::size_t off = t * part;
+        if (off >= bytes) break;
+        ts.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off,
+                        std::min(part, bytes - off));
+        });
+    }
+    std::memcpy(dst, src, std::min(part, bytes));
+    for (auto& t : ts) t.join();
+}
 
 // CRS tile pack of an inline sparse group for post tiles of tileN neurons
 // (layout in kernels.cuh, GroupDev::tpack).  With words == nullptr only the
@@ -218,11 +257,11 @@ struct DeviceEngine::Impl {
     // Host copy of the raster: drained arenas, in order.  A flush switches the
     // device to the other arena and drains the full one on a copy stream from
     // a helper thread, so the simulation keeps running during the copy.
-    std::vector<std::pair<std::unique_ptr<std::int32_t[]>, std::size_t>> hostChunks;
+    std::vector<std::pair<std::shared_ptr<std::int32_t>, std::size_t>> hostChunks;
     int* arenaSelDev = nullptr;
     int arenaSel = 0;
     cudaStream_t copyStream = nullptr;
-    static constexpr std::size_t kPinnedInts = std::size_t(1) << 23;  // 32 MB per stage
+    static constexpr std::size_t kPinnedInts = std::size_t(1) << 22;  // 16 MB per stage
     std::int32_t* pinned[2] = {nullptr, nullptr};
     std::thread copier;
     void join_copier() {
@@ -1015,7 +1054,7 @@ void DeviceEngine::Impl::flush_raster(bool wait) {
     arenaSel ^= 1;
     CK(cudaMemcpy(arenaSelDev, &arenaSel, sizeof(int), cudaMemcpyHostToDevice));
     if (cur > 0 && !rasterDiscarded) {
-        auto chunk = std::unique_ptr<std::int32_t[]>(new std::int32_t[static_cast<std::size_t>(cur)]);
+        auto chunk = host_events(static_cast<std::size_t>(cur));
         std::int32_t* dst = chunk.get();
         hostChunks.emplace_back(std::move(chunk), static_cast<std::size_t>(cur));
         const int* src = raster.arena[full];
@@ -1033,7 +1072,7 @@ void DeviceEngine::Impl::flush_raster(bool wait) {
                 const std::size_t len = off < total ? std::min(piece, total - off) : 0;
                 if (len)
                     cudaMemcpyAsync(stage[k], src + off, len * 4, cudaMemcpyDeviceToHost, cs);
-                if (prevLen) std::memcpy(dst + prevOff, stage[k ^ 1], prevLen * 4);
+                if (prevLen) parallel_copy(dst + prevOff, stage[k ^ 1], prevLen * 4);
                 cudaStreamSynchronize(cs);
                 prevOff = off;
                 prevLen = len;
@@ -1414,6 +1453,16 @@ void DeviceEngine::collect_raster(std::vector<std::int32_t>& counts,
         std::copy(c.first.get(), c.first.get() + c.second, neurons.data() + at);
         at += c.second;
     }
+}
+
+std::int64_t DeviceEngine::drain_raster() {
+    auto& m = *impl_;
+    CK(cudaSetDevice(m.cfg.device));
+    if (!m.rasterDiscarded) m.flush_raster(true);
+    m.join_copier();
+    std::int64_t n = 0;
+    for (const auto& c : m.hostChunks) n += static_cast<std::int64_t>(c.second);
+    return n;
 }
 
 void DeviceEngine::discard_raster() {

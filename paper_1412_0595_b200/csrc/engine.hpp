@@ -150,6 +150,7 @@ public:
     // (step, pop, neuron) order.
     void collect_raster(std::vector<std::int32_t>& counts, std::vector<std::int32_t>& neurons);
     void discard_raster();
+    std::int64_t drain_raster();  // synchronous flush to the host store; events held
     void spike_totals(std::vector<std::int64_t>& perPop);
 
     // Neurons of population pop held by this process: [lo, lo + n) of

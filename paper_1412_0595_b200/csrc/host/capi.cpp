@@ -783,6 +783,13 @@ int ssb_spike_counts(ssb_sim* sim, int64_t* counts, int32_t n_pops) {
     });
 }
 
+int ssb_raster_drain(ssb_sim* sim, int64_t* n_events) {
+    return on_sim(sim, [&](ssb::SimCore& c) {
+        const std::int64_t n = c.engine().drain_raster();
+        if (n_events) *n_events = n;
+    });
+}
+
 int ssb_raster_discard(ssb_sim* sim) {
     return on_sim(sim, [&](ssb::SimCore& c) { c.engine().discard_raster(); });
 }

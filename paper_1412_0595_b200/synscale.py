@@ -608,6 +608,13 @@ class Simulation:
     def discard_raster(self) -> None:
         self._check(lib.ssb_raster_discard(self._h))
 
+    def drain_raster(self) -> int:
+        """Waits for the issued steps and moves every recorded event to host
+        memory; returns the number of events now held on the host."""
+        n = C.c_int64()
+        self._check(lib.ssb_raster_drain(self._h, C.byref(n)))
+        return n.value
+
     def device_bytes(self) -> int:
         return int(lib.ssb_device_bytes(self._h))
 

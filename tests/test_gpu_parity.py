@@ -397,3 +397,20 @@ def test_concurrent_simulations_of_different_sizes(golden):
         r = sim.finish()
         assert specs.sha(r.raster.step, r.raster.population, r.raster.neuron) == \
             golden["runs"][name]["raster_sha"]
+
+
+def test_raster_drain_midway_keeps_results(golden):
+    """ssb_raster_drain moves events to the host mid-run; the finished raster
+    is unchanged (the bench's end-to-end leg relies on it)."""
+    spec, mode = GOLDEN["cfg2_100ms"]()
+    sim = gpu_sim(spec, mode, window=64)
+    held = 0
+    for n in (100, 300, 250):
+        sim.step(n)
+        h = sim.drain_raster()
+        assert h >= held
+        held = h
+    r = sim.finish()
+    assert len(r.raster) >= held
+    assert specs.sha(r.raster.step, r.raster.population, r.raster.neuron) == \
+        golden["runs"]["cfg2_100ms"]["raster_sha"]
