@@ -156,6 +156,8 @@ bool kernel_attributes(const std::string& name, int& regs, int& sharedBytes, int
     cudaFuncAttributes a;
     cudaError_t e;
     if (name == "condlif_window") e = cudaFuncGetAttributes(&a, ssbk::condlif_window_kernel);
+    else if (name == "izh_window") e = cudaFuncGetAttributes(&a, ssbk::izh_window_kernel);
+    else if (name == "gaussian_window") e = cudaFuncGetAttributes(&a, ssbk::gaussian_window_kernel);
     else if (name == "poisson_window") e = cudaFuncGetAttributes(&a, ssbk::poisson_window_kernel);
     else if (name == "dense_window") e = cudaFuncGetAttributes(&a, ssbk::dense_window_kernel);
     else if (name == "dense_window_warp")
@@ -310,15 +312,16 @@ struct DeviceEngine::Impl {
     template <typename F>
     void launch(const std::string& name, F&& f) {
         ++enqueued;
+        const std::string what = "launch of " + name;
         if (!cfg.profile) {
             f();
-            CK(cudaGetLastError());
+            check(cudaGetLastError(), what.c_str());
             return;
         }
         cudaEvent_t a = take_event(), b = take_event();
         CK(cudaEventRecord(a, stream));
         f();
-        CK(cudaGetLastError());
+        check(cudaGetLastError(), what.c_str());
         CK(cudaEventRecord(b, stream));
         pending.push_back({name, {a, b}});
     }
@@ -430,7 +433,6 @@ int DeviceEngine::Impl::choose_block(int n, const std::function<std::int64_t(int
     if (n <= 256) return single;  // one block; extra threads serve the parallel phases
     // a forced block size applies to the multi-block populations (the ones
     // whose update the occupancy model sizes)
-    if (cfg.blockSize > 0) return std::min(round_up(cfg.blockSize, 32), 1024);
     int regs = 32, shared = 0, maxThreads = 1024;
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, kernelFn) == cudaSuccess) {
@@ -440,6 +442,8 @@ int DeviceEngine::Impl::choose_block(int n, const std::function<std::int64_t(int
     } else {
         cudaGetLastError();
     }
+    if (cfg.blockSize > 0)
+        return std::min(round_up(cfg.blockSize, 32), std::min(1024, maxThreads / 32 * 32));
     const synscale::DeviceSpec dev = synscale::device_preset("sm100");
     auto smem = [&](int bs) { return static_cast<std::int64_t>(shared) + smemFor(bs); };
     auto fits = [&](int bs) { return smem(bs) <= 220 * 1024; };
@@ -545,11 +549,12 @@ int DeviceEngine::Impl::plan_stage(const HostNet& net, int pi, int tileN, ssbk::
         const std::int64_t inBudget =
             std::max<std::int64_t>(16 * 1024, std::min<std::int64_t>(single ? 96 * 1024 : 64 * 1024,
                                                                      200 * 1024 - off));
-        C = static_cast<int>(std::clamp<std::int64_t>(inBudget / (2LL * tileN * 4), 4, 64));
+        const int planes = P.kind == kIzhikevich ? 3 : 2;  // ex, ih (+ noise)
+        C = static_cast<int>(std::clamp<std::int64_t>(inBudget / (planes * tileN * 4LL), 4, 64));
         C = std::min(C, W);
         off = align(off, 16);
         offIn = static_cast<int>(off);
-        off += 2LL * C * tileN * 4;
+        off += static_cast<std::int64_t>(planes) * C * tileN * 4;
         offBits = -1;
         if (single && P.nwords <= 32) {
             offBits = static_cast<int>(off);
@@ -588,11 +593,6 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         if (static_cast<int>(q.size()) != nPops) cyclic = true;
         order = cyclic ? std::vector<int>() : q;
     }
-    for (const auto& p : net.pops)
-        if (p.kind == kIzhikevich)
-            throw synscale::SpecError(
-                "population '" + p.name +
-                "': the Izhikevich model is not implemented by the B200 engine yet");
     stepMode = cyclic || cfg.forceStepMode;
     if (stepMode) {
         order.resize(nPops);
@@ -641,7 +641,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
                 for (int gi : gl)
                     if (!net.groups[gi].dense) P.sparseInline = true;
         }
-        if (hp.kind == kCondLif) {
+        if (hp.kind == kCondLif || hp.kind == kIzhikevich) {
             // tile size from the occupancy model (registers of the kernel +
             // this tile's shared-memory plan, 1 KB per-block reservation)
             ssbk::StageAcc tmp[2];
@@ -651,7 +651,9 @@ void DeviceEngine::Impl::build(const HostNet& net) {
                 [&](int tn) {
                     return plan_stage(net, pi, tn, tmp, tmpIn, tmpC, tmpBits) + 1024;
                 },
-                reinterpret_cast<const void*>(&ssbk::condlif_window_kernel));
+                hp.kind == kIzhikevich
+                    ? reinterpret_cast<const void*>(&ssbk::izh_window_kernel)
+                    : reinterpret_cast<const void*>(&ssbk::condlif_window_kernel));
             P.grid = (hp.n + P.tileN - 1) / P.tileN;
             // a single-block population gets extra threads for the parallel phases
             P.block = P.grid == 1 ? P.tileN * std::max(1, 256 / P.tileN) : P.tileN;
@@ -703,6 +705,24 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         if (hp.kind == kCondLif) {
             std::vector<float> v0(n, hp.eLeak);  // engine.cpp:199
             CK(cudaMemcpyAsync(d.v, v0.data(), n * sizeof(float), cudaMemcpyHostToDevice, stream));
+            CK(cudaStreamSynchronize(stream));
+        }
+        if (hp.kind == kIzhikevich) {
+            // engine.cpp:164-183: v = -65, u = b v (fp32); noise stream state
+            std::vector<float> v0(n, -65.0f), u0(n);
+            for (std::size_t i = 0; i < n; ++i) u0[i] = hp.b[i] * v0[i];
+            CK(cudaMemcpyAsync(d.v, v0.data(), n * sizeof(float), cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(d.u, u0.data(), n * sizeof(float), cudaMemcpyHostToDevice, stream));
+            d.ia = upload<float>(hp.a.data(), n);
+            d.ib = upload<float>(hp.b.data(), n);
+            d.ic = upload<float>(hp.c.data(), n);
+            d.id = upload<float>(hp.d.data(), n);
+            d.bias = upload<double>(hp.bias.data(), n);
+            d.amp = upload<double>(hp.noise.data(), n);
+            d.spare = alloc<double>(1);
+            d.hasSpare = alloc<int>(1);
+            d.noiseIn = alloc<float>(static_cast<std::size_t>(Wmax) * n);
+            d.draws = alloc<unsigned long long>(static_cast<std::size_t>(Wmax) * n + 2);
             CK(cudaStreamSynchronize(stream));
         }
         for (int a = 0; a < 2; ++a)
@@ -764,7 +784,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         if (g.dense) {
             G.W = upload<float>(g.W, static_cast<std::size_t>(g.nPre) * g.nPost);
         } else {
-            G.segTile = post.kind == kCondLif ? post.tileN : 256;
+            G.segTile = post.kind != kPoisson ? post.tileN : 256;
             G.nTiles = (g.nPost + G.segTile - 1) / G.segTile;
             G.g = upload<float>(g.g, static_cast<std::size_t>(g.nnz));
             G.ind = upload<int>(g.ind, static_cast<std::size_t>(g.nnz));
@@ -784,7 +804,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             G.seg = seg;
             // static CRS tile pack when the post kernel's plan stages one
             bool packed = false;
-            for (int a = 0; a < 2 && post.kind == kCondLif; ++a)
+            for (int a = 0; a < 2 && post.kind != kPoisson; ++a)
                 for (int k = 0; k < post.acc[a].ng; ++k)
                     if (post.accGroups[a][k] == static_cast<int>(gi) &&
                         post.stage[a].g[k].tpackWords > 0)
@@ -878,6 +898,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     };
     allow(reinterpret_cast<const void*>(&ssbk::condlif_window_kernel), std::max(maxSmem, 4096));
+    allow(reinterpret_cast<const void*>(&ssbk::izh_window_kernel), std::max(maxSmem, 4096));
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_warp_kernel), kWarpRingBytes);
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_pipe_kernel), ring_smem());
     if (const char* e = std::getenv("SSB_DENSE_KERNEL")) usePipe = std::string(e) == "pipe";
@@ -921,11 +942,22 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t s) {
         const ssbk::PopDev& K = P.kdev[b];
         const bool wide = is_wide(P.grid, P.smemBytes);
         if (wide) before_wide(s);
-        launch("condlif_window:" + P.name, [&] {
-            ssbk::condlif_window_kernel<<<P.grid, P.block, P.smemBytes, s>>>(
-                K, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk,
-                P.offIn, P.offBits);
-        });
+        if (P.kind == kIzhikevich) {
+            launch("gaussian_window:" + P.name, [&] {
+                ssbk::gaussian_window_kernel<<<1, 320, 0, s>>>(K, W);
+            });
+            launch("izh_window:" + P.name, [&] {
+                ssbk::izh_window_kernel<<<P.grid, P.block, P.smemBytes, s>>>(
+                    K, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk,
+                    P.offIn, P.offBits);
+            });
+        } else {
+            launch("condlif_window:" + P.name, [&] {
+                ssbk::condlif_window_kernel<<<P.grid, P.block, P.smemBytes, s>>>(
+                    K, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk,
+                    P.offIn, P.offBits);
+            });
+        }
         if (P.grid > 1 && !P.sharded) {
             const int bs = std::min(1024, round_up(P.nwords, 32));
             launch("compact_window:" + P.name, [&] {

@@ -329,7 +329,8 @@ def build_izhikevich_net(nNeurons: int, nConn: int, excFraction: float, gScale: 
 def validate(spec: NetworkSpec) -> List[Tuple[str, str]]:
     """validate (reference network.hpp:89-91): every violation as (field, message)."""
     buf = C.create_string_buffer(1 << 16)
-    n = lib.ssb_validate(NetDesc(spec).ptr, buf, len(buf))
+    desc = NetDesc(spec)  # keeps the flattened arrays alive across the call
+    n = lib.ssb_validate(desc.ptr, buf, len(buf))
     if n < 0:
         raise SpecError(buf.value.decode())
     out = []

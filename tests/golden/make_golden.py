@@ -54,8 +54,10 @@ def run_ref(spec, mode):
         "head": [[int(a), int(b), int(c)] for a, b, c in zip(step[:40], pop[:40], neu[:40])],
     }
     for pi, p in enumerate(spec.populations):
-        out["state_sha"][p.name] = {f: specs.sha(sim.state(pi, f)) for f in
-                                    ("v", "gExc", "gInh", "excIn", "inhIn", "nanFlag")}
+        fields = ("v", "gExc", "gInh", "excIn", "inhIn", "nanFlag")
+        if p.model == S.ModelKind.Izhikevich:
+            fields = ("v", "u", "excIn", "inhIn", "nanFlag")
+        out["state_sha"][p.name] = {f: specs.sha(sim.state(pi, f)) for f in fields}
     for gi, g in enumerate(spec.synapses):
         kind, m = sim.group(gi)
         out["groups"][g.name] = [kind, specs.sha(*(m if kind == "sparse" else (m,)))]
@@ -89,6 +91,9 @@ def main():
         "cfg2_fromspec_100ms": (specs.config_spec(2, 100.0)[0], S.StorageMode.FromSpec),
         "chain_100ms": (specs.chain_spec(100.0), S.StorageMode.FromSpec),
         "recurrent_200ms": (specs.recurrent_lif_spec(), S.StorageMode.FromSpec),
+        "izh_1000_1000ms": (specs.izh_spec(), S.StorageMode.FromSpec),
+        "izh_1000_dense_300ms": (specs.izh_spec(duration_ms=300.0), S.StorageMode.ForceDense),
+        "izh_ff_200ms": (specs.izh_ff_spec(), S.StorageMode.FromSpec),
     }.items():
         print("reference run", name, flush=True)
         runs[name] = run_ref(spec, mode)
@@ -109,6 +114,20 @@ def main():
     np.savez_compressed(os.path.join(OUT, "condlif_kat.npz"), v=np.array(v, np.float32),
                         gExc=np.array(ge, np.float32), gInh=np.array(gi, np.float32),
                         step=step, pop=pop, neuron=neu)
+
+    # Izhikevich known answer (test_engine.cpp:79-111): one bias-driven neuron,
+    # per-step v / u from the reference.
+    one = specs.single_izh_spec()
+    d = S.NetDesc(one)
+    sim = O.CpuSim(d.ptr, one, 0, ref=True)
+    v, u = [], []
+    for _ in range(sim.steps_total()):
+        sim.step(1)
+        v.append(sim.state(0, "v")[0])
+        u.append(sim.state(0, "u")[0])
+    step, pop, neu = sim.finish()
+    np.savez_compressed(os.path.join(OUT, "izh_kat.npz"), v=np.array(v, np.float32),
+                        u=np.array(u, np.float32), step=step, pop=pop, neuron=neu)
 
     with open(os.path.join(OUT, "golden.json"), "w") as f:
         json.dump(gold, f, indent=1, sort_keys=True)

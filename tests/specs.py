@@ -120,3 +120,46 @@ def bits_equal(a: np.ndarray, b: np.ndarray) -> bool:
     if not np.array_equal(na, nb):
         return False
     return bool(np.array_equal(a[~na].view(np.uint32), b[~nb].view(np.uint32)))
+
+
+def izh_spec(n: int = 1000, n_conn: int = 100, duration_ms: float = 1000.0,
+             storage=S.StorageKind.Sparse, g_scale: float = 6.0, seed: int = 1) -> S.NetworkSpec:
+    """The reference's acceptance network (acceptance_main.cpp:139-163):
+    recurrent Izhikevich population, noise-driven, dt 1 ms."""
+    opt = S.IzhBuildOptions(dtMs=1.0, durationMs=duration_ms, storage=storage)
+    return S.build_izhikevich_net(n, n_conn, 0.8, g_scale, seed, opt)
+
+
+def single_izh_spec(bias: float = 10.0, duration_ms: float = 300.0, seed: int = 99) -> S.NetworkSpec:
+    """test_engine.cpp:21-41: one regular-spiking neuron with a constant bias."""
+    spec = S.NetworkSpec(dtMs=1.0, durationMs=duration_ms, globalSeed=seed)
+    spec.populations = [S.NeuronPopulation("n", 1, S.ModelKind.Izhikevich, 3, S.IzhikevichParams(
+        a=[0.02], b=[0.2], c=[-65.0], d=[8.0], noiseAmplitude=[0.0], biasCurrent=[bias]))]
+    return spec
+
+
+def izh_ff_spec(duration_ms: float = 200.0) -> S.NetworkSpec:
+    """Feed-forward mix (windowed path): Poisson -> noisy Izhikevich (odd size, so
+    Gaussian pairs straddle steps) -> CondLif, dense and sparse groups."""
+    import numpy as _np
+    rng = _np.random.default_rng(5)
+    n = 1001
+    r = rng.random(n)
+    spec = S.NetworkSpec(dtMs=0.5, durationMs=duration_ms, globalSeed=23)
+    spec.populations = [
+        S.NeuronPopulation("src", 200, S.ModelKind.PoissonSource, 1, S.PoissonParams(30.0)),
+        S.NeuronPopulation("izh", n, S.ModelKind.Izhikevich, 2, S.IzhikevichParams(
+            a=[float(x) for x in 0.02 + 0.08 * r], b=[float(x) for x in 0.25 - 0.05 * r],
+            c=[-65.0] * n, d=[float(x) for x in 2.0 + 6.0 * r], noiseAmplitude=[3.0] * n,
+            biasCurrent=[float(x) for x in 2.0 * r])),
+        S.NeuronPopulation("out", 100, S.ModelKind.CondLif, 3, S.CondLifParams()),
+    ]
+    spec.synapses = [
+        S.SynapseGroupSpec("in_e", "src", "izh", S.SynapseSign.Excitatory, 100,
+                           S.WeightDist.uniform(0.0, 3.0), 1.0, S.StorageKind.Sparse),
+        S.SynapseGroupSpec("in_i", "src", "izh", S.SynapseSign.Inhibitory, 50,
+                           S.WeightDist.uniform(0.0, 2.0), 1.0, S.StorageKind.Dense, 100, 100),
+        S.SynapseGroupSpec("fwd", "izh", "out", S.SynapseSign.Excitatory, 20,
+                           S.WeightDist.uniform(0.0, 0.05), 1.0, S.StorageKind.Dense),
+    ]
+    return spec

@@ -51,6 +51,9 @@ GOLDEN = {
     "cfg2_fromspec_100ms": lambda: (specs.config_spec(2, 100.0)[0], S.StorageMode.FromSpec),
     "chain_100ms": lambda: (specs.chain_spec(100.0), S.StorageMode.FromSpec),
     "recurrent_200ms": lambda: (specs.recurrent_lif_spec(), S.StorageMode.FromSpec),
+    "izh_1000_1000ms": lambda: (specs.izh_spec(), S.StorageMode.FromSpec),
+    "izh_1000_dense_300ms": lambda: (specs.izh_spec(duration_ms=300.0), S.StorageMode.ForceDense),
+    "izh_ff_200ms": lambda: (specs.izh_ff_spec(), S.StorageMode.FromSpec),
 }
 
 
@@ -70,6 +73,36 @@ def test_runs_match_reference_golden(golden, name, window):
             if p.model == S.ModelKind.PoissonSource and f in ("v", "gExc", "gInh"):
                 continue
             assert specs.sha(sim.pull(pi, f)) == h, (p.name, f)
+
+
+def test_izhikevich_kat_per_step():
+    """test_engine.cpp:79-111 on the device: per-step bitwise v / u of one
+    bias-driven Izhikevich neuron (the noise stream is drawn, times 0)."""
+    kat = np.load(os.path.join(os.path.dirname(__file__), "golden", "izh_kat.npz"))
+    spec = specs.single_izh_spec()
+    sim = gpu_sim(spec)
+    for t in range(sim.steps_total()):
+        sim.step(1)
+        assert sim.pull(0, "v")[0] == kat["v"][t] and sim.pull(0, "u")[0] == kat["u"][t], t
+    r = sim.finish()
+    assert np.array_equal(r.raster.step, kat["step"]) and len(kat["step"]) > 0
+
+
+@pytest.mark.parametrize("window", [1, 64])
+def test_izhikevich_noise_stream_matches_oracle(oracle_mod, window):
+    """Noisy Izhikevich inputs (Gaussian pairs straddling steps, odd sizes),
+    stepwise state against the oracle."""
+    spec = specs.izh_ff_spec(60.0)
+    g = gpu_sim(spec, window=window)
+    o = cpu_sim(oracle_mod, spec)
+    for t in range(0, 120, 40):
+        g.step(40)
+        o.step(40)
+        for pi, p in enumerate(spec.populations):
+            fields = ("v", "u", "excIn", "inhIn") if p.model == S.ModelKind.Izhikevich else \
+                (("v", "gExc", "gInh", "excIn", "inhIn") if p.model == S.ModelKind.CondLif else ())
+            for f in fields:
+                assert specs.bits_equal(g.pull(pi, f), o.state(pi, f)), (t, p.name, f)
 
 
 def test_condlif_kat_per_step():

@@ -6,6 +6,8 @@
 * re-hosts the reference's own known-answer tests for the step path
   (test_engine.cpp:183-359, 361-400).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -45,7 +47,8 @@ def test_gen_fixed_outdegree_matches_golden(oracle_mod, golden):
 
 
 @pytest.mark.parametrize("name", ["cfg1_1000ms", "cfg2_100ms", "cfg3_20ms", "cfg1_sparse_300ms",
-                                  "cfg2_fromspec_100ms", "chain_100ms", "recurrent_200ms"])
+                                  "cfg2_fromspec_100ms", "chain_100ms", "recurrent_200ms",
+                                  "izh_1000_1000ms", "izh_1000_dense_300ms", "izh_ff_200ms"])
 def test_oracle_runs_match_golden(oracle_mod, golden, name):
     g = golden["runs"][name]
     spec, mode = {
@@ -56,6 +59,9 @@ def test_oracle_runs_match_golden(oracle_mod, golden, name):
         "cfg2_fromspec_100ms": (specs.config_spec(2, 100.0)[0], S.StorageMode.FromSpec),
         "chain_100ms": (specs.chain_spec(100.0), S.StorageMode.FromSpec),
         "recurrent_200ms": (specs.recurrent_lif_spec(), S.StorageMode.FromSpec),
+        "izh_1000_1000ms": (specs.izh_spec(), S.StorageMode.FromSpec),
+        "izh_1000_dense_300ms": (specs.izh_spec(duration_ms=300.0), S.StorageMode.ForceDense),
+        "izh_ff_200ms": (specs.izh_ff_spec(), S.StorageMode.FromSpec),
     }[name]
     sim, (step, pop, neu) = _run(oracle_mod, spec, mode)
     assert step.size == g["n_events"]
@@ -68,6 +74,20 @@ def test_oracle_runs_match_golden(oracle_mod, golden, name):
     for gi, grp in enumerate(spec.synapses):
         kind, m = sim.group(gi)
         assert [kind, specs.sha(*(m if kind == "sparse" else (m,)))] == g["groups"][grp.name]
+
+
+def test_izhikevich_kat_per_step(oracle_mod):
+    """test_engine.cpp:79-111: per-step bitwise v, u of one bias-driven
+    Izhikevich neuron, against the reference's values."""
+    kat = np.load(os.path.join(os.path.dirname(__file__), "golden", "izh_kat.npz"))
+    spec = specs.single_izh_spec()
+    d = S.NetDesc(spec)
+    sim = oracle_mod.CpuSim(d.ptr, spec, 0)
+    for t in range(sim.steps_total()):
+        sim.step(1)
+        assert sim.state(0, "v")[0] == kat["v"][t] and sim.state(0, "u")[0] == kat["u"][t], t
+    step, pop, neu = sim.finish()
+    assert np.array_equal(step, kat["step"]) and len(step) > 0
 
 
 def test_condlif_kat_per_step(oracle_mod):
