@@ -181,14 +181,19 @@ bool kernel_attributes(const std::string& name, int& regs, int& sharedBytes, int
 // ---------------------------------------------------------------------------
 
 struct DeviceEngine::Impl {
+    // window-buffer sets: every window of a graph launch gets its own set of
+    // spike lists / bitmasks / buffered inputs, so no window waits for an
+    // earlier one's consumers to free a buffer (launches serialise anyway)
+    static constexpr int kMaxSets = 16;
+    int nSets = 2;
     struct PopRt {
         int kind = 0, n = 0, nwords = 0;
         int block = 0, grid = 0;
         bool sparseInline = false;  // needs a dynamic shared tile
         ssbk::PopDev dev{};             // state + window buffer set 0
         ssbk::AccDev acc[2]{};          // accumulator plans (buffer set 0 views)
-        ssbk::PopDev devb[2]{};         // per window-buffer set b
-        ssbk::AccDev accb[2][2]{};      // [b][sign]
+        ssbk::PopDev devb[kMaxSets]{};     // per window-buffer set b
+        ssbk::AccDev accb[kMaxSets][2]{};  // [b][sign]
         std::vector<int> prePops;       // populations whose spikes of the same window feed it
         std::vector<int> consumers;     // populations reading its spike lists
         ssbk::StageAcc stage[2]{};  // shared-memory staging plan (condlif)
@@ -205,8 +210,8 @@ struct DeviceEngine::Impl {
         // bits / lists (n = nGlobal) that consumers and the raster read.
         bool sharded = false;
         int nGlobal = 0, lo = 0, shardChunk = 0, nwGlobal = 0;
-        ssbk::PopDev kdev[2]{};
-        uint32_t* gathered[2] = {nullptr, nullptr};  // [world][W][nwords]
+        ssbk::PopDev kdev[kMaxSets]{};
+        uint32_t* gathered[kMaxSets] = {};  // [world][W][nwords]
     };
     struct LaunchStat {
         std::string name;
@@ -278,11 +283,11 @@ struct DeviceEngine::Impl {
     std::vector<cudaEvent_t> eventPool;
 
     template <typename T>
-    T* alloc(std::size_t count) {
+    T* alloc(std::size_t count, bool zero = true) {
         void* p = nullptr;
         const std::size_t b = std::max<std::size_t>(count, 1) * sizeof(T);
         CK(cudaMalloc(&p, b));
-        CK(cudaMemsetAsync(p, 0, b, stream));
+        if (zero) CK(cudaMemsetAsync(p, 0, b, stream));
         allocations.push_back(p);
         bytes += static_cast<std::int64_t>(b);
         return static_cast<T*>(p);
@@ -309,29 +314,49 @@ struct DeviceEngine::Impl {
     int enqueued = 0;                 // kernels put on the stream by enqueue_window
     std::map<int, int> kernelsPerWindow;
 
+    // Diagnostic timeline (env SSB_TIMELINE=<file>): no graphs, the normal
+    // multi-stream schedule, events around every launch on its own stream;
+    // harvest() appends "name start_us end_us" lines (relative to the first
+    // launch) to the file.
+    std::string timelinePath;
+    cudaEvent_t timelineBase = nullptr;
+    cudaStream_t launchStream = nullptr;  // stream of the launches being enqueued
+    bool timed() const { return cfg.profile || !timelinePath.empty(); }
+
     template <typename F>
     void launch(const std::string& name, F&& f) {
         ++enqueued;
         const std::string what = "launch of " + name;
-        if (!cfg.profile) {
+        if (!timed()) {
             f();
             check(cudaGetLastError(), what.c_str());
             return;
         }
+        cudaStream_t ls = launchStream && !timelinePath.empty() ? launchStream : stream;
         cudaEvent_t a = take_event(), b = take_event();
-        CK(cudaEventRecord(a, stream));
+        if (!timelinePath.empty() && !timelineBase) {
+            CK(cudaEventCreate(&timelineBase));
+            CK(cudaEventRecord(timelineBase, ls));
+        }
+        CK(cudaEventRecord(a, ls));
         f();
         check(cudaGetLastError(), what.c_str());
-        CK(cudaEventRecord(b, stream));
+        CK(cudaEventRecord(b, ls));
         pending.push_back({name, {a, b}});
     }
 
     void harvest() {
         if (pending.empty()) return;
-        CK(cudaStreamSynchronize(stream));
+        CK(cudaDeviceSynchronize());
+        FILE* tl = timelinePath.empty() ? nullptr : std::fopen(timelinePath.c_str(), "a");
         for (auto& [name, ev] : pending) {
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, ev.first, ev.second));
+            if (tl) {
+                float t0 = 0.f;
+                CK(cudaEventElapsedTime(&t0, timelineBase, ev.first));
+                std::fprintf(tl, "%s %.3f %.3f\n", name.c_str(), t0 * 1e3, (t0 + ms) * 1e3);
+            }
             auto& s = stats[name];
             s.name = name;
             s.launches += 1;
@@ -339,6 +364,7 @@ struct DeviceEngine::Impl {
             eventPool.push_back(ev.first);
             eventPool.push_back(ev.second);
         }
+        if (tl) std::fclose(tl);
         pending.clear();
     }
 
@@ -347,7 +373,16 @@ struct DeviceEngine::Impl {
     int plan_stage(const HostNet& net, int pi, int tileN, ssbk::StageAcc out[2], int& offIn,
                    int& C, int& offBits) const;
     void build(const HostNet& net);
-    void enqueue_pop(int pi, int W, int b, cudaStream_t s);
+    void enqueue_pop(int pi, int W, int b, cudaStream_t s) { enqueue_pop(pi, W, b, s, s, s); }
+    // sg: group kernels filling buffered inputs; sm: the population update;
+    // sp: compaction / exchange (the window's lists for consumers)
+    void enqueue_pop(int pi, int W, int b, cudaStream_t sg, cudaStream_t sm, cudaStream_t sp);
+    void edge(cudaStream_t from, cudaStream_t to) {
+        if (from == to) return;
+        cudaEvent_t e = capture_event();
+        CK(cudaEventRecord(e, from));
+        CK(cudaStreamWaitEvent(to, e, 0));
+    }
     void assemble_compact(int pi, int W, int b, cudaStream_t s);
     std::int64_t pre_launch(int W, int M);
     void post_launch(int W, int M, std::int64_t add);
@@ -358,7 +393,7 @@ struct DeviceEngine::Impl {
     void release();
 
     // multi-window graphs
-    ssbk::RasterDev rasterb[2]{};
+    ssbk::RasterDev rasterb[kMaxSets]{};
     std::vector<cudaStream_t> auxStreams;
     std::vector<cudaEvent_t> capEvents;
     std::size_t evUsed = 0;
@@ -667,6 +702,21 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         }
     }
 
+    // windows per graph launch (overlap across windows needs an acyclic graph)
+    graphWindows = stepMode ? 1 : 4;
+    if (const char* e = std::getenv("SSB_GRAPH_WINDOWS"))
+        if (!stepMode) graphWindows = std::clamp(std::atoi(e), 1, kMaxSets);
+    {
+        // The host runs at most kRing launches ahead of the last cursor it has
+        // seen, so the arena must hold kRing + 1 launches of worst-case events
+        // (every neuron spiking every step); beyond 4G events (16 GB per arena,
+        // two arenas) shrink the launch.
+        const std::int64_t perWin = static_cast<std::int64_t>(Wmax) * totalNeurons;
+        while (graphWindows > 1 && (kRing + 1) * perWin * graphWindows > (std::int64_t(1) << 32))
+            graphWindows /= 2;
+    }
+    nSets = std::clamp(graphWindows, 2, kMaxSets);
+
     // population buffers
     for (int pi = 0; pi < nPops; ++pi) {
         auto& P = pops[pi];
@@ -728,24 +778,25 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         for (int a = 0; a < 2; ++a)
             if (P.acc[a].mode == ssbk::kAccBuffered)
                 P.acc[a].buf = alloc<float>(static_cast<std::size_t>(Wmax + 1) * n);
-        // second window-buffer set: windows m and m+1 of one graph are in flight
-        // at once (spike lists, bitmasks, counts, buffered inputs)
-        P.devb[0] = d;
-        P.devb[1] = d;
-        P.devb[1].bits = alloc<uint32_t>(static_cast<std::size_t>(Wmax) * P.nwords);
-        P.devb[1].list = alloc<int>(static_cast<std::size_t>(Wmax) * n);
-        P.devb[1].count = alloc<int>(static_cast<std::size_t>(Wmax));
-        for (int a = 0; a < 2; ++a) {
-            P.accb[0][a] = P.acc[a];
-            P.accb[1][a] = P.acc[a];
-            if (P.acc[a].mode == ssbk::kAccBuffered)
-                P.accb[1][a].buf = alloc<float>(static_cast<std::size_t>(Wmax + 1) * n);
+        // further window-buffer sets (the windows of one graph are in flight
+        // together): spike lists, bitmasks, counts, buffered inputs
+        for (int b = 0; b < nSets; ++b) {
+            P.devb[b] = d;
+            if (b > 0) {
+                P.devb[b].bits = alloc<uint32_t>(static_cast<std::size_t>(Wmax) * P.nwords);
+                P.devb[b].list = alloc<int>(static_cast<std::size_t>(Wmax) * n);
+                P.devb[b].count = alloc<int>(static_cast<std::size_t>(Wmax));
+            }
+            for (int a = 0; a < 2; ++a) {
+                P.accb[b][a] = P.acc[a];
+                if (b > 0 && P.acc[a].mode == ssbk::kAccBuffered)
+                    P.accb[b][a].buf = alloc<float>(static_cast<std::size_t>(Wmax + 1) * n);
+            }
+            P.kdev[b] = P.devb[b];
         }
-        P.kdev[0] = P.devb[0];
-        P.kdev[1] = P.devb[1];
         if (P.sharded) {
             const std::size_t ng = static_cast<std::size_t>(P.nGlobal);
-            for (int b = 0; b < 2; ++b) {
+            for (int b = 0; b < nSets; ++b) {
                 P.gathered[b] = alloc<uint32_t>(static_cast<std::size_t>(world) * Wmax * P.nwords);
                 auto& g = P.devb[b];
                 g.n = P.nGlobal;
@@ -754,7 +805,6 @@ void DeviceEngine::Impl::build(const HostNet& net) {
                 g.list = alloc<int>(static_cast<std::size_t>(Wmax) * ng);
                 g.count = alloc<int>(static_cast<std::size_t>(Wmax));
             }
-            P.dev.n = P.n;
         }
     }
     for (const auto& g : net.groups) {
@@ -832,7 +882,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             for (int k = 0; k < P.acc[a].ng; ++k) {
                 const int gi = P.accGroups[a][k];
                 P.acc[a].g[k] = groupDev[gi];
-                for (int b = 0; b < 2; ++b) {
+                for (int b = 0; b < nSets; ++b) {
                     ssbk::GroupDev G = groupDev[gi];
                     G.preList = pops[net.groups[gi].pre].devb[b].list;
                     G.preCnt = pops[net.groups[gi].pre].devb[b].count;
@@ -847,16 +897,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         raster.count[pi] = pops[pi].dev.count;
         raster.list[pi] = pops[pi].dev.list;
     }
-    // windows per graph launch (overlap across windows needs an acyclic graph)
-    graphWindows = stepMode ? 1 : 4;
-    if (const char* e = std::getenv("SSB_GRAPH_WINDOWS"))
-        if (!stepMode) graphWindows = std::max(1, std::atoi(e));
-    // The host runs at most kRing launches ahead of the last cursor it has
-    // seen, so the arena must hold kRing + 1 launches of worst-case events
-    // (every neuron spiking every step); beyond ~2G events shrink the launch.
+    // raster arena capacity for kRing + 1 launches of worst-case events
     const std::int64_t perWindow = static_cast<std::int64_t>(Wmax) * totalNeurons;
-    while (graphWindows > 1 && (kRing + 1) * perWindow * graphWindows > (std::int64_t(1) << 31))
-        graphWindows /= 2;
     const std::int64_t perLaunch = perWindow * graphWindows;
     rasterCap = cfg.rasterCapacity > 0
                     ? cfg.rasterCapacity
@@ -864,8 +906,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     rasterCap = std::max(rasterCap, (kRing + 1) * perLaunch);
     CK(cudaMallocHost(&ringVal, kRing * sizeof(long long)));
     for (auto& e : ringEv) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    raster.arena[0] = alloc<int>(static_cast<std::size_t>(rasterCap));
-    raster.arena[1] = alloc<int>(static_cast<std::size_t>(rasterCap));
+    raster.arena[0] = alloc<int>(static_cast<std::size_t>(rasterCap), false);
+    raster.arena[1] = alloc<int>(static_cast<std::size_t>(rasterCap), false);
     arenaSelDev = alloc<int>(1);
     raster.arenaSel = arenaSelDev;
     CK(cudaStreamCreateWithFlags(&copyStream, cudaStreamNonBlocking));
@@ -876,7 +918,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     raster.stepCounter = alloc<long long>(1);
     raster.windowCounter = alloc<long long>(1);
     raster.doneCounter = alloc<unsigned>(1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < nSets; ++b) {
         rasterb[b] = raster;
         for (int pi = 0; pi < nPops; ++pi) {
             rasterb[b].count[pi] = pops[pi].devb[b].count;
@@ -884,7 +926,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         }
     }
     // capture streams: one per population, one for deliver + raster
-    auxStreams.resize(nPops + 1);
+    auxStreams.resize(3 * nPops + 1);
     for (auto& s : auxStreams) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
 
     // kernels with large dynamic shared tiles (the limit is per function and
@@ -902,23 +944,29 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_warp_kernel), kWarpRingBytes);
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_pipe_kernel), ring_smem());
     if (const char* e = std::getenv("SSB_DENSE_KERNEL")) usePipe = std::string(e) == "pipe";
+    if (const char* e = std::getenv("SSB_TIMELINE")) timelinePath = e;
     CK(cudaStreamSynchronize(stream));
 }
 
 // One population's kernels for one window on stream s, window-buffer set b.
-void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t s) {
+void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cudaStream_t sm,
+                                     cudaStream_t sp) {
     auto& P = pops[pi];
     const ssbk::PopDev& D = P.devb[b];
     if (P.kind == kPoisson) {
+        launchStream = sm;
         launch("poisson_window:" + P.name, [&] {
             const int bitsBytes = W * P.nwords * 4;
             const int inSmem = bitsBytes <= 32 * 1024;
-            ssbk::poisson_window_kernel<<<1, 320, inSmem ? bitsBytes : 0, s>>>(
+            ssbk::poisson_window_kernel<<<1, 320, inSmem ? bitsBytes : 0, sm>>>(
                 D, W, P.acc[0].mode, P.acc[1].mode, inSmem);
         });
+        edge(sm, sp);
         return;
     }
     if (P.n > 0) {
+        launchStream = sg;
+        bool groups = false;
         for (int a = 0; a < 2; ++a) {
             const auto& A = P.accb[b][a];
             if (A.mode != ssbk::kAccBuffered) continue;
@@ -926,58 +974,68 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t s) {
                 const auto& G = A.g[k];
                 const int gi = P.accGroups[a][k];
                 float* out = A.buf + P.n;  // row w = 1
+                groups = true;
                 if (G.dense || G.fullRows) {
                     ssbk::GroupDev D = G;
                     if (!G.dense) D.W = G.g;  // full CRS rows = dense rows
-                    launch_dense(D, groupMeta[gi].name, "dense_window:", out, P.n, 1, W, k == 0, s);
+                    launch_dense(D, groupMeta[gi].name, "dense_window:", out, P.n, 1, W, k == 0, sg);
                 } else {
                     dim3 grid(G.nTiles, W);
                     launch("sparse_window:" + groupMeta[gi].name, [&] {
-                        ssbk::sparse_window_kernel<<<grid, G.segTile, 0, s>>>(
+                        ssbk::sparse_window_kernel<<<grid, G.segTile, 0, sg>>>(
                             G, out, P.n, 1, k == 0);
                     });
                 }
             }
         }
+        if (groups) edge(sg, sm);
+        launchStream = sm;
         const ssbk::PopDev& K = P.kdev[b];
         const bool wide = is_wide(P.grid, P.smemBytes);
-        if (wide) before_wide(s);
+        if (wide) before_wide(sm);
         if (P.kind == kIzhikevich) {
             launch("gaussian_window:" + P.name, [&] {
-                ssbk::gaussian_window_kernel<<<1, 320, 0, s>>>(K, W);
+                ssbk::gaussian_window_kernel<<<1, 320, 0, sm>>>(K, W);
             });
             launch("izh_window:" + P.name, [&] {
-                ssbk::izh_window_kernel<<<P.grid, P.block, P.smemBytes, s>>>(
+                ssbk::izh_window_kernel<<<P.grid, P.block, P.smemBytes, sm>>>(
                     K, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk,
                     P.offIn, P.offBits);
             });
         } else {
             launch("condlif_window:" + P.name, [&] {
-                ssbk::condlif_window_kernel<<<P.grid, P.block, P.smemBytes, s>>>(
+                ssbk::condlif_window_kernel<<<P.grid, P.block, P.smemBytes, sm>>>(
                     K, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk,
                     P.offIn, P.offBits);
             });
         }
+        // the next wide kernel may start right after the update: compaction
+        // (on sp) feeds only this window's consumers
+        if (wide) after_wide(sm);
+        edge(sm, sp);
+        launchStream = sp;
         if (P.grid > 1 && !P.sharded) {
             const int bs = std::min(1024, round_up(P.nwords, 32));
             launch("compact_window:" + P.name, [&] {
-                ssbk::compact_window_kernel<<<W, bs, 0, s>>>(K.bits, P.nwords, P.n, K.list, K.count);
+                ssbk::compact_window_kernel<<<W, bs, 0, sp>>>(K.bits, P.nwords, P.n, K.list, K.count);
             });
         }
-        if (wide) after_wide(s);
+    } else {
+        edge(sm, sp);
     }
     if (P.sharded) {
         // the window's exchange: every rank's local bits, in rank order
         if (comm)
             comm->allgather_u32(P.kdev[b].bits, P.gathered[b],
-                                static_cast<std::size_t>(W) * P.nwords, s);
-        if (!virtualShard) assemble_compact(pi, W, b, s);  // virtual: after the shard copies
+                                static_cast<std::size_t>(W) * P.nwords, sp);
+        if (!virtualShard) assemble_compact(pi, W, b, sp);  // virtual: after the shard copies
     }
 }
 
 // Global bitmask and ordered spike lists of a split population from the
 // gathered local bitmasks (rank order = ascending neuron order).
 void DeviceEngine::Impl::assemble_compact(int pi, int W, int b, cudaStream_t s) {
+    launchStream = s;
     auto& P = pops[pi];
     const ssbk::PopDev& D = P.devb[b];
     const int bs = std::min(1024, round_up(P.nwGlobal, 32));
@@ -994,6 +1052,7 @@ void DeviceEngine::Impl::assemble_compact(int pi, int W, int b, cudaStream_t s) 
 // Poisson targets: inputs of the next step from the last step's spikes), then
 // the window's raster.
 void DeviceEngine::Impl::enqueue_tail(int W, int b, cudaStream_t s) {
+    launchStream = s;
     for (auto& P : pops) {
         for (int a = 0; a < 2; ++a) {
             const auto& A = P.accb[b][a];
@@ -1028,7 +1087,9 @@ void DeviceEngine::Impl::enqueue_tail(int W, int b, cudaStream_t s) {
 void DeviceEngine::Impl::enqueue_windows(int W, int M) {
     const int nPops = static_cast<int>(pops.size());
     const bool multi = !cfg.profile && !serial;  // profile / virtual shards: one stream
-    const int rs = nPops;
+    // (the diagnostic timeline keeps the multi-stream schedule)
+    // streams: 3 per population (groups, update, compaction), then the raster
+    const int rs = 3 * nPops;
     auto S = [&](int idx) { return multi ? auxStreams[idx] : stream; };
     evUsed = 0;
     multiStream = multi;
@@ -1050,17 +1111,26 @@ void DeviceEngine::Impl::enqueue_windows(int W, int M) {
     std::vector<std::vector<cudaEvent_t>> kdone(nPops, std::vector<cudaEvent_t>(M, nullptr));
     std::vector<cudaEvent_t> rdone(M, nullptr);
     for (int m = 0; m < M; ++m) {
-        const int b = m & 1;
+        const int b = m % nSets;
         for (int pi : order) {
             auto& P = pops[pi];
-            for (int q : P.prePops) after(pi, kdone[q][m]);
-            if (m >= 2) {  // buffer set b was last read by window m-2's consumers
-                for (int c : P.consumers) after(pi, kdone[c][m - 2]);
-                after(pi, rdone[m - 2]);
+            // extra streams only where they carry work (a graph's branches share
+            // a few hardware queues: unused parallelism costs false dependencies)
+            const int sm = 3 * pi + 1;
+            const int sg = P.acc[0].mode == ssbk::kAccBuffered || P.acc[1].mode == ssbk::kAccBuffered
+                               ? 3 * pi : sm;
+            const int sp = (P.grid > 1 && P.n > 0) || P.sharded ? 3 * pi + 2 : sm;
+            for (int x : {sg, sm}) {
+                for (int q : P.prePops) after(x, kdone[q][m]);
+                if (m >= nSets) {  // buffer set b was last read by window m-nSets's consumers
+                    for (int c : P.consumers) after(x, kdone[c][m - nSets]);
+                    after(x, rdone[m - nSets]);
+                    after(x, kdone[pi][m - nSets]);
+                }
+                if (stepMode && m >= 1) after(x, rdone[m - 1]);
             }
-            if (stepMode && m >= 1) after(pi, rdone[m - 1]);
-            enqueue_pop(pi, W, b, S(pi));
-            kdone[pi][m] = mark(pi);
+            enqueue_pop(pi, W, b, S(sg), S(sm), S(sp));
+            kdone[pi][m] = mark(sp);
         }
         for (int pi = 0; pi < nPops; ++pi) after(rs, kdone[pi][m]);
         enqueue_tail(W, b, S(rs));
@@ -1149,8 +1219,8 @@ void DeviceEngine::Impl::post_launch(int W, int M, std::int64_t add) {
 
 void DeviceEngine::Impl::run_windows(int W, int M) {
     const std::int64_t add = pre_launch(W, M);
-    const int key = W * 64 + M;
-    if (cfg.useGraphs && !cfg.profile && !serial) {
+    const int key = W * 64 + M;  // M <= kMaxSets < 64
+    if (cfg.useGraphs && !timed() && !serial) {
         auto it = graphs.find(key);
         if (it == graphs.end()) {
             cudaGraph_t g;
@@ -1247,7 +1317,7 @@ void DeviceEngine::lockstep(int W) {
     std::vector<std::int64_t> add(R);
     for (int r = 0; r < R; ++r) add[r] = all[r]->pre_launch(W, 1);
     Impl& m0 = *impl_;
-    const int b = static_cast<int>(m0.windowsLaunched & 1);
+    const int b = static_cast<int>(m0.windowsLaunched % m0.nSets);
     for (auto* m : all) {
         m->enqueued = 0;
         m->evUsed = 0;
@@ -1320,16 +1390,26 @@ void DeviceEngine::step(std::int64_t n) {
         return;
     }
     const std::int64_t full = static_cast<std::int64_t>(m.Wmax) * m.graphWindows;
-    while (n > 0) {
-        if (m.graphWindows > 1 && n >= full) {
-            m.run_windows(m.Wmax, m.graphWindows);
-            n -= full;
-        } else {
+    while (n >= full && m.graphWindows > 1) {
+        m.run_windows(m.Wmax, m.graphWindows);
+        n -= full;
+    }
+    if (n <= 0) return;
+    if (m.graphWindows == 1) {
+        while (n > 0) {
             const int W = static_cast<int>(std::min<std::int64_t>(m.Wmax, n));
             m.run_windows(W, 1);
             n -= W;
         }
+        return;
     }
+    // the rest as ceil(n / Wmax) near-equal windows in at most two graph
+    // launches (cached like the full ones), so a remainder still overlaps
+    // populations across windows instead of running window by window
+    const int k = static_cast<int>((n + m.Wmax - 1) / m.Wmax);
+    const int w = static_cast<int>(n / k), r = static_cast<int>(n % k);
+    if (k - r > 0) m.run_windows(w, k - r);
+    if (r > 0) m.run_windows(w + 1, r);
 }
 
 void DeviceEngine::sync() {

@@ -1,0 +1,32 @@
+"""Per-launch timeline of config 3 windows (diagnostic): SSB_TIMELINE mode
+(no graphs, the normal multi-stream schedule, events around every launch)."""
+import collections
+import os
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
+path = os.path.join(tempfile.mkdtemp(), "tl.txt")
+os.environ["SSB_TIMELINE"] = path
+import specs  # noqa: E402
+from paper_1412_0595_b200 import synscale as S  # noqa: E402
+
+W = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+spec, mode = specs.config_spec(3, 400.0)
+sim = S.Simulation(spec, mode, S.EngineOptions(window=W))
+sim.step(W * 4)
+sim.sync()
+open(path, "w").close()
+sim.step(W * 8)
+sim.sync()
+sim.kernel_stats()  # harvest
+rows = [l.split() for l in open(path)]
+rows = [(n, float(a), float(b)) for n, a, b in rows]
+t0 = min(r[1] for r in rows)
+rows = [(n, a - t0, b - t0) for n, a, b in rows]
+span = max(r[2] for r in rows)
+print(f"{len(rows)} launches, {span:.1f} us for 8 windows -> {span / 8:.1f} us/window, "
+      f"{span / 8 / W * 1e3:.1f} ns/step")
+for n, a, b in sorted(rows, key=lambda r: r[1])[:int(os.environ.get("TL_ROWS", "40"))]:
+    print(f"{n:28s} {a:9.1f} {b:9.1f} {b - a:8.1f}")
