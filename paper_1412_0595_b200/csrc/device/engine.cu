@@ -703,7 +703,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     }
 
     // windows per graph launch (overlap across windows needs an acyclic graph)
-    graphWindows = stepMode ? 1 : 4;
+    graphWindows = stepMode ? 1 : kMaxSets;
     if (const char* e = std::getenv("SSB_GRAPH_WINDOWS"))
         if (!stepMode) graphWindows = std::clamp(std::atoi(e), 1, kMaxSets);
     {

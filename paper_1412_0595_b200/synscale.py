@@ -454,7 +454,7 @@ class Simulation:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # lib is None during interpreter shutdown
             lib.ssb_destroy(h)
             self._h = None
 
