@@ -581,9 +581,14 @@ int DeviceEngine::Impl::plan_stage(const HostNet& net, int pi, int tileN, ssbk::
                 off += static_cast<std::int64_t>(S.entCap) * 4;
             }
         }
-        const std::int64_t inBudget =
-            std::max<std::int64_t>(16 * 1024, std::min<std::int64_t>(single ? 96 * 1024 : 64 * 1024,
-                                                                     200 * 1024 - off));
+        // phase-A input planes: more steps per chunk = fewer block barriers
+        // (env SSB_IN_KB overrides the multi-block budget, for sweeps)
+        static const std::int64_t multiKb = [] {
+            const char* e = std::getenv("SSB_IN_KB");
+            return e ? std::max(16, std::atoi(e)) : 96;
+        }();
+        const std::int64_t inBudget = std::max<std::int64_t>(
+            16 * 1024, std::min<std::int64_t>(single ? 96 * 1024 : multiKb * 1024, 200 * 1024 - off));
         const int planes = P.kind == kIzhikevich ? 3 : 2;  // ex, ih (+ noise)
         C = static_cast<int>(std::clamp<std::int64_t>(inBudget / (planes * tileN * 4LL), 4, 64));
         C = std::min(C, W);
