@@ -13,7 +13,8 @@ if len(sys.argv) > 1:  # child: one M
     M = int(sys.argv[1])
     n = 256 * 64
     spec, mode = specs.config_spec(3, (n * 2 + 512) * 0.1)
-    sim = S.Simulation(spec, mode, S.EngineOptions(window=256))
+    sim = S.Simulation(spec, mode, S.EngineOptions(window=256,
+                                                   blockSize=int(os.environ.get("GS_BS", "0"))))
     sim.step(n)
     sim.sync()
     st = torch.cuda.ExternalStream(sim.stream())
@@ -23,8 +24,10 @@ if len(sys.argv) > 1:  # child: one M
     e1.record(st)
     e1.synchronize()
     ms = e0.elapsed_time(e1)
-    print(f"M={M:2d}: {ms * 1e3 / 64:7.1f} us/window, {ms * 1e3 / n:6.3f} us/step", flush=True)
+    print(f"M={M:2d} kc_block={sim.block_size('kc')}: {ms * 1e3 / 64:7.1f} us/window, "
+          f"{ms * 1e3 / n:6.3f} us/step", flush=True)
 else:
-    for M in (1, 2, 4, 8, 16):
+    for M in ([int(x) for x in os.environ["GS_M"].split(",")] if "GS_M" in os.environ
+              else (1, 2, 4, 8, 16)):
         env = dict(os.environ, SSB_GRAPH_WINDOWS=str(M))
         subprocess.run([sys.executable, __file__, str(M)], env=env)
