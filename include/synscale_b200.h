@@ -240,6 +240,9 @@ SSB_API int ssb_shard_group(const ssb_net_desc* net, int32_t storage_mode, int32
                             size_t errlen);
 /* NCCL unique id for ssb_engine_opts.comm_id (loads libnccl; no GPU work). */
 SSB_API int ssb_comm_unique_id(uint8_t* out128, char* err, size_t errlen);
+/* Self-test of the exchange on one device: a one-rank communicator, the
+ * all-gather and the sum the split engine issues (graph-captured and not). */
+SSB_API int ssb_comm_selftest(int32_t device, char* err, size_t errlen);
 SSB_API uint64_t ssb_mem_dense_elements(uint64_t n_pre, uint64_t n_post); /* matrix.cpp:180 */
 
 /* ---- standalone device kernels -------------------------------------------- */

@@ -131,6 +131,7 @@ _SIGNATURES = {
     "ssb_shard_group": (C.c_int, [P(ssb_net_desc), _i32, _i32, _i32, _i32, _i32, P(_i32), P(_i32),
                                   P(_i32), P(_i64), P(_f32), P(_i32), P(_i64), _i64, _cp, _sz]),
     "ssb_comm_unique_id": (C.c_int, [P(_u8), _cp, _sz]),
+    "ssb_comm_selftest": (C.c_int, [_i32, _cp, _sz]),
     "ssb_mem_sparse_elements": (_u64, [_u64, _u64]),
     "ssb_mem_dense_elements": (_u64, [_u64, _u64]),
     "ssb_propagate_dense": (C.c_int, [P(_f32), _i32, _i32, P(_i32), _i64, P(_f32), _i64, _cp, _sz]),

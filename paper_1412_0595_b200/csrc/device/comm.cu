@@ -5,6 +5,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../engine.hpp"
 #include "comm.hpp"
@@ -84,6 +85,56 @@ void Comm::allgather_u32(const void* send, void* recv, std::size_t count, cudaSt
 void Comm::allreduce_sum_u64(void* buf, std::size_t count, cudaStream_t s) {
     nck(nccl().allReduce(buf, buf, count, ncclUint64, ncclSum, static_cast<ncclComm_t>(comm_), s),
         "ncclAllReduce");
+}
+
+}  // namespace ssb
+
+namespace ssb {
+
+void comm_selftest(int device) {
+    auto ck = [](cudaError_t e, const char* what) {
+        if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    const auto id = nccl_unique_id();
+    Comm comm(1, 0, id.data());
+    cudaStream_t s;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    constexpr int n = 1000;
+    std::uint32_t* send = nullptr;
+    std::uint32_t* recv = nullptr;
+    unsigned long long* sum = nullptr;
+    ck(cudaMalloc(&send, n * 4), "cudaMalloc");
+    ck(cudaMalloc(&recv, n * 4), "cudaMalloc");
+    ck(cudaMalloc(&sum, 8), "cudaMalloc");
+    std::vector<std::uint32_t> h(n), back(n);
+    for (int i = 0; i < n; ++i) h[i] = 0x9e3779b9u * static_cast<std::uint32_t>(i + 1);
+    ck(cudaMemcpy(send, h.data(), n * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
+    const unsigned long long seven = 7;
+    ck(cudaMemcpy(sum, &seven, 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+    comm.allgather_u32(send, recv, n, s);
+    comm.allreduce_sum_u64(sum, 1, s);
+    // the same all-gather captured in a graph, as the window graphs issue it
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    ck(cudaMemsetAsync(recv, 0, n * 4, s), "cudaMemsetAsync");
+    ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    comm.allgather_u32(send, recv, n, s);
+    ck(cudaStreamEndCapture(s, &g), "cudaStreamEndCapture");
+    ck(cudaGraphInstantiate(&ge, g, 0), "cudaGraphInstantiate");
+    ck(cudaGraphLaunch(ge, s), "cudaGraphLaunch");
+    ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    unsigned long long got = 0;
+    ck(cudaMemcpy(back.data(), recv, n * 4, cudaMemcpyDeviceToHost), "cudaMemcpy");
+    ck(cudaMemcpy(&got, sum, 8, cudaMemcpyDeviceToHost), "cudaMemcpy");
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaFree(send);
+    cudaFree(recv);
+    cudaFree(sum);
+    cudaStreamDestroy(s);
+    if (back != h) throw DeviceError("NCCL self-test: all-gather returned wrong words");
+    if (got != 7) throw DeviceError("NCCL self-test: all-reduce returned a wrong sum");
 }
 
 }  // namespace ssb

@@ -111,6 +111,9 @@ HostNet shard_net(const HostNet& net, const ShardPlan& plan, int rank, ShardStor
 
 // NCCL unique id for a new communicator (libnccl loaded on first use).
 std::array<unsigned char, 128> comm_unique_id();
+// One-rank communicator on `device`: all-gather and sum, plain and inside a
+// captured CUDA graph; throws DeviceError on any mismatch or NCCL failure.
+void comm_selftest(int device);
 
 struct KernelStat {
     std::string name;

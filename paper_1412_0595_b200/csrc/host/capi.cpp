@@ -531,6 +531,10 @@ int ssb_shard_group(const ssb_net_desc* net, int32_t storage_mode, int32_t group
     });
 }
 
+int ssb_comm_selftest(int32_t device, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { ssb::comm_selftest(device); });
+}
+
 int ssb_comm_unique_id(uint8_t* out128, char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
         const auto id = ssb::comm_unique_id();

@@ -796,6 +796,12 @@ def shard_group(spec: NetworkSpec, group: Union[int, str], world: int, rank: int
     return "sparse", (vals, ind, rs)
 
 
+def comm_selftest(device: int = 0) -> None:
+    """Runs the split engine's NCCL calls on a one-rank communicator (raises on failure)."""
+    err = _err()
+    _raise(lib.ssb_comm_selftest(device, err, len(err)), err.value.decode())
+
+
 def comm_unique_id() -> bytes:
     """NCCL unique id for EngineOptions.commId (rank 0 creates, the caller
     broadcasts it, e.g. with torch.distributed.broadcast_object_list)."""

@@ -447,3 +447,9 @@ def test_raster_drain_midway_keeps_results(golden):
     assert len(r.raster) >= held
     assert specs.sha(r.raster.step, r.raster.population, r.raster.neuron) == \
         golden["runs"]["cfg2_100ms"]["raster_sha"]
+
+
+def test_nccl_exchange_selftest():
+    """The split engine's collectives (dlopen'd libnccl, one-rank communicator):
+    all-gather and sum, plain and captured in a CUDA graph."""
+    S.comm_selftest(0)
