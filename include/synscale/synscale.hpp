@@ -14,6 +14,7 @@
 
 #include <array>
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <span>
@@ -346,6 +347,35 @@ private:
 };
 
 RunResult run(const NetworkSpec& spec, StorageMode mode = StorageMode::FromSpec);
+// B200 extension: run with engine options.
+RunResult run(const NetworkSpec& spec, StorageMode mode, const EngineOptions& options);
+
+// ---- calibration sweep (reference calibration.hpp:12-42), the hot path's caller ----
+// Cells run as independent device simulations driven by `parallelism` host
+// threads (each Simulation owns its streams, so cells overlap on the GPU).
+
+struct SweepRow {
+    std::int32_t nConn = 0;
+    double gScale = 0.0;
+    double avgSpike = 0.0;
+    std::int64_t sumNaNs = 0;
+    bool failed = false;
+    std::string error;
+};
+
+using TemplateBuilder = std::function<NetworkSpec(std::int32_t nConn, double gScale)>;
+
+struct SweepRequest {
+    std::vector<std::int32_t> nConnValues;
+    std::vector<double> gScaleValues;
+    std::string targetPopulation;
+    int parallelism = 1;
+    StorageMode storage = StorageMode::FromSpec;
+    std::function<void(const SweepRow&, std::size_t done, std::size_t total)> onCell;
+    EngineOptions engine;  // B200 extension
+};
+
+std::vector<SweepRow> sweep(const TemplateBuilder& builder, const SweepRequest& req);
 
 // ---- occupancy model (reference occupancy.hpp:10-70) -----------------------
 

@@ -225,6 +225,17 @@ SSB_API int ssb_build_group(const ssb_net_desc* net, int32_t storage_mode, int32
                             char* err, size_t errlen);
 SSB_API uint64_t ssb_mem_sparse_elements(uint64_t nnz, uint64_t n_post); /* matrix.cpp:176 */
 
+/* ---- calibration sweep (calibration.cpp:16-86) ------------------------------ */
+/* Runs n_cells independent networks (one sweep cell each, built by the caller
+ * from its template) to their end on the GPU, `parallelism` at a time, and
+ * records the target population's avgSpike and the run's sumNaNs per cell.  A
+ * cell that fails gets failed[i] = 1, avg_spike NaN, sum_nans -1 and its error
+ * text in errors + i * err_stride (may be NULL). */
+SSB_API int ssb_sweep(const ssb_net_desc* const* cells, int32_t n_cells, int32_t storage_mode,
+                      const char* target_population, int32_t parallelism,
+                      const ssb_engine_opts* opts, double* avg_spike, int64_t* sum_nans,
+                      int32_t* failed, char* errors, size_t err_stride, char* err, size_t errlen);
+
 /* ---- multi-GPU decomposition (host, no GPU needed) ------------------------- */
 /* Neuron ranges of a world of `world` ranks: bounds[p*(world+1) + r] = first
  * neuron of rank r in population p (r = world: the size), or -1 for every r

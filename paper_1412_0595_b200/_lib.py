@@ -127,6 +127,8 @@ _SIGNATURES = {
                                           P(_f32), _cp, _sz]),
     "ssb_build_group": (C.c_int, [P(ssb_net_desc), _i32, _i32, P(_i32), P(_i32), P(_i32), P(_i64),
                                   P(_f32), P(_i32), P(_i64), _i64, _cp, _sz]),
+    "ssb_sweep": (C.c_int, [P(P(ssb_net_desc)), _i32, _i32, _cp, _i32, P(ssb_engine_opts), P(_dbl),
+                            P(_i64), P(_i32), _cp, _sz, _cp, _sz]),
     "ssb_shard_plan": (C.c_int, [P(ssb_net_desc), _i32, _i32, P(_i64), _cp, _sz]),
     "ssb_shard_group": (C.c_int, [P(ssb_net_desc), _i32, _i32, _i32, _i32, _i32, P(_i32), P(_i32),
                                   P(_i32), P(_i64), P(_f32), P(_i32), P(_i64), _i64, _cp, _sz]),

@@ -1,6 +1,7 @@
 // capi.cpp — extern "C" boundary (include/synscale_b200.h).  Converts flat
 // descriptors to the C++ model, runs everything behind try/catch and maps
 // SpecError -> SSB_ERR_SPEC, anything else -> SSB_ERR_INTERNAL.
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -465,6 +466,41 @@ int ssb_build_group(const ssb_net_desc* net, int32_t storage_mode, int32_t group
                 std::memcpy(values, s->gValues.data(), s->gValues.size() * sizeof(float));
                 std::memcpy(post_ind, s->postInd.data(), s->postInd.size() * sizeof(int32_t));
                 std::memcpy(row_start, s->rowStart.data(), s->rowStart.size() * sizeof(int64_t));
+            }
+        }
+    });
+}
+
+int ssb_sweep(const ssb_net_desc* const* cells, int32_t n_cells, int32_t storage_mode,
+              const char* target_population, int32_t parallelism, const ssb_engine_opts* opts,
+              double* avg_spike, int64_t* sum_nans, int32_t* failed, char* errors,
+              size_t err_stride, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (n_cells < 1) throw SpecError("sweep needs at least one cell");
+        SweepRequest req;
+        for (int32_t i = 0; i < n_cells; ++i) req.nConnValues.push_back(i);  // cell index
+        req.gScaleValues = {0.0};
+        req.targetPopulation = str(target_population);
+        req.parallelism = parallelism;
+        req.storage = to_mode(storage_mode);
+        const ssb::EngineConfig c = to_config(opts);
+        req.engine.device = c.device;
+        req.engine.window = c.window;
+        req.engine.blockSize = c.blockSize;
+        req.engine.blockPolicy = c.blockPolicy;
+        req.engine.useGraphs = c.useGraphs;
+        req.engine.heavyPreThreshold = c.heavyPreThreshold;
+        req.engine.rasterCapacity = c.rasterCapacity;
+        const std::vector<SweepRow> rows =
+            sweep([&](std::int32_t i, double) { return to_spec(cells[i]); }, req);
+        for (int32_t i = 0; i < n_cells; ++i) {
+            const SweepRow& r = rows[static_cast<std::size_t>(i)];
+            avg_spike[i] = r.avgSpike;
+            sum_nans[i] = r.sumNaNs;
+            failed[i] = r.failed ? 1 : 0;
+            if (errors && err_stride) {
+                char* dst = errors + static_cast<std::size_t>(i) * err_stride;
+                std::snprintf(dst, err_stride, "%s", r.error.c_str());
             }
         }
     });

@@ -177,9 +177,11 @@ RunResult Simulation::finish() {
     return m.core.run_result();
 }
 
-RunResult run(const NetworkSpec& spec, StorageMode mode) {
+RunResult run(const NetworkSpec& spec, StorageMode mode) { return run(spec, mode, EngineOptions{}); }
+
+RunResult run(const NetworkSpec& spec, StorageMode mode, const EngineOptions& options) {
     const auto t0 = std::chrono::steady_clock::now();
-    Simulation sim(spec, mode);
+    Simulation sim(spec, mode, options);
     RunResult r = sim.finish();
     r.wallTimeMs =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

@@ -759,6 +759,81 @@ def build_group(spec: NetworkSpec, group: Union[int, str],
     return "sparse", (vals, ind, rs)
 
 
+# ---- calibration sweep (reference calibration.hpp:12-42) -------------------------------
+
+
+@dataclass
+class SweepRow:
+    nConn: int = 0
+    gScale: float = 0.0
+    avgSpike: float = 0.0
+    sumNaNs: int = 0
+    failed: bool = False
+    error: str = ""
+
+
+@dataclass
+class SweepRequest:
+    nConnValues: Sequence[int] = ()
+    gScaleValues: Sequence[float] = ()
+    targetPopulation: str = ""
+    parallelism: int = 1
+    storage: "StorageMode" = None
+    onCell: Optional[object] = None  # called (row, done, total) after each cell, in order
+    engine: Optional["EngineOptions"] = None  # B200 extension
+
+
+def sweep(builder, req: SweepRequest) -> List[SweepRow]:
+    """sweep (reference calibration.cpp:16-86): every (nConn, gScale) grid cell
+    (duplicates collapsed, ascending) built by builder(nConn, gScale) and run to
+    its end on the GPU, req.parallelism cells at a time.  A cell whose build or
+    run fails is recorded (failed, avgSpike NaN, sumNaNs -1), not raised."""
+    if builder is None:
+        raise SpecError("sweep needs a network builder")
+    if not req.nConnValues:
+        raise SpecError("sweep needs at least one nConn value")
+    if not req.gScaleValues:
+        raise SpecError("sweep needs at least one gScale value")
+    if not req.targetPopulation:
+        raise SpecError("sweep needs a target population name")
+    if any(not np.isfinite(g) for g in req.gScaleValues):
+        raise SpecError("sweep gScale values must be finite")
+    rows, descs, which = [], [], []
+    for n in sorted(set(int(x) for x in req.nConnValues)):
+        for g in sorted(set(float(x) for x in req.gScaleValues)):
+            row = SweepRow(n, g)
+            try:
+                descs.append(NetDesc(builder(n, g)))
+                which.append(len(rows))
+            except Exception as exc:  # noqa: BLE001 -- recorded like the reference
+                row.failed, row.error, row.avgSpike, row.sumNaNs = True, str(exc), float("nan"), -1
+            rows.append(row)
+    if descs:
+        k = len(descs)
+        arr = (C.POINTER(L.ssb_net_desc) * k)(*[C.pointer(d.desc) for d in descs])
+        avg = np.empty(k, np.float64)
+        nans = np.empty(k, np.int64)
+        failed = np.empty(k, np.int32)
+        stride = 512
+        errs = C.create_string_buffer(k * stride)
+        opts = (req.engine or EngineOptions()).to_c()
+        mode = int(req.storage if req.storage is not None else StorageMode.FromSpec)
+        err = _err()
+        _raise(lib.ssb_sweep(arr, k, mode, req.targetPopulation.encode(), max(1, req.parallelism),
+                             C.byref(opts), avg.ctypes.data_as(C.POINTER(C.c_double)),
+                             _lptr(nans), _iptr(failed), errs, stride, err, len(err)),
+               err.value.decode())
+        for j, i in enumerate(which):
+            r = rows[i]
+            r.avgSpike, r.sumNaNs, r.failed = float(avg[j]), int(nans[j]), bool(failed[j])
+            if r.failed:
+                r.error = errs.raw[j * stride:(j + 1) * stride].split(b"\0", 1)[0].decode()
+    if req.onCell:
+        for d, r in enumerate(rows, 1):
+            req.onCell(r, d, len(rows))
+    return rows
+
+
 def shard_plan(spec: NetworkSpec, world: int, minSize: int = 0) -> Dict[str, Optional[List[int]]]:
     """Neuron ranges of a world of `world` ranks per population (None: whole,
     replicated on every rank), as the engine splits it (host, no GPU)."""

@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "synscale/calibration.hpp"
 #include "synscale/engine.hpp"
 #include "synscale/io.hpp"
 #include "synscale/network.hpp"
@@ -158,7 +159,44 @@ static void fault_injection_and_storage() {
     CHECK(a.size() > 1000);
 }
 
+static void calibration_sweep() {
+    // calibration.cpp:16-86 through the drop-in header: grid collapsed and
+    // sorted, failures recorded per row, cells on worker threads
+    TemplateBuilder builder = [](std::int32_t nConn, double gScale) {
+        MBodyBuildOptions o;
+        o.dtMs = 0.5;
+        o.durationMs = 40.0;
+        if (nConn == 7) throw SpecError("builder rejects nConn 7");
+        return build_mbody_net(100, 20, 1000, 100,
+                               {{"pn_kc", gScale}, {"pn_lhi", 1.0}, {"lhi_kc", 0.1},
+                                {"kc_dn", 0.03}},
+                               static_cast<std::uint64_t>(nConn), o);
+    };
+    SweepRequest req;
+    req.nConnValues = {3, 7, 3};
+    req.gScaleValues = {2.0, 1.0};
+    req.targetPopulation = "kc";
+    req.parallelism = 2;
+    std::size_t calls = 0;
+    req.onCell = [&](const SweepRow&, std::size_t, std::size_t total) {
+        ++calls;
+        CHECK(total == 4);
+    };
+    const std::vector<SweepRow> rows = sweep(builder, req);
+    CHECK(rows.size() == 4);
+    CHECK(calls == 4);
+    CHECK(rows[0].nConn == 3 && rows[0].gScale == 1.0 && rows[1].gScale == 2.0);
+    CHECK(!rows[0].failed && !rows[1].failed && rows[2].failed && rows[3].failed);
+    CHECK(rows[2].sumNaNs == -1 && std::isnan(rows[2].avgSpike));
+    // the sweep's rate is the run's rate
+    const RunResult direct = run(builder(3, 2.0), StorageMode::FromSpec);
+    CHECK(rows[1].avgSpike == direct.avgSpike.at("kc"));
+    req.targetPopulation = "nope";
+    CHECK(sweep(builder, req)[0].failed);
+}
+
 int main() {
+    calibration_sweep();
     conductance_kat();
     propagate_examples();
     fault_injection_and_storage();

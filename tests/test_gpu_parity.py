@@ -453,3 +453,27 @@ def test_nccl_exchange_selftest():
     """The split engine's collectives (dlopen'd libnccl, one-rank communicator):
     all-gather and sum, plain and captured in a CUDA graph."""
     S.comm_selftest(0)
+
+
+def test_sweep_cells_match_oracle(oracle_mod):
+    """The calibration sweep on the GPU (calibration.cpp:16-86): every cell's
+    target rate and NaN count equal the oracle's run of the same network;
+    cells run 3 at a time on their own streams."""
+    def builder(n, g):
+        spec = specs.mbody_spec(1000, 0.5, 50.0)
+        pk = spec.synapses[spec.group_index("pn_kc")]
+        pk.outDegree = n
+        pk.gScale = g
+        return spec
+    req = S.SweepRequest([100, 300, 500], [0.5, 1.5], "kc", parallelism=3,
+                         storage=S.StorageMode.ForceDense)
+    rows = S.sweep(builder, req)
+    assert len(rows) == 6 and not any(r.failed for r in rows)
+    kc = 2
+    for r in rows:
+        spec = builder(r.nConn, r.gScale)
+        o = cpu_sim(oracle_mod, spec, S.StorageMode.ForceDense)
+        o.finish()
+        assert r.avgSpike == float(o.rates()[kc]), (r.nConn, r.gScale)
+        assert r.sumNaNs == o.sum_nans()
+    assert len({r.avgSpike for r in rows}) > 1

@@ -251,3 +251,37 @@ def test_raster_csv_and_avg_spike():
     for bad in (("missing", 1000.0), ("a", 0.0), ("a", -5.0)):
         with pytest.raises(S.SpecError):
             S.avg_spike(r, *bad)
+
+
+def _sweep_builder(n, g):
+    import specs
+    spec = specs.mbody_spec(1000, 0.5, 20.0)
+    pk = spec.synapses[spec.group_index("pn_kc")]
+    pk.outDegree = n
+    pk.gScale = g
+    if n == 13:
+        raise ValueError("builder refuses 13")
+    return spec
+
+
+def test_sweep_grid_validation_and_failure_rows():
+    """sweep (calibration.cpp:16-86) host logic: argument errors raise; the grid
+    collapses duplicates and sorts; a failing builder or run is recorded in its
+    row (here every run fails without a GPU, like a run that throws)."""
+    with pytest.raises(S.SpecError):
+        S.sweep(_sweep_builder, S.SweepRequest([], [1.0], "kc"))
+    with pytest.raises(S.SpecError):
+        S.sweep(_sweep_builder, S.SweepRequest([10], [], "kc"))
+    with pytest.raises(S.SpecError):
+        S.sweep(_sweep_builder, S.SweepRequest([10], [1.0], ""))
+    with pytest.raises(S.SpecError):
+        S.sweep(_sweep_builder, S.SweepRequest([10], [float("inf")], "kc"))
+    if S.device_count() > 0:
+        return
+    seen = []
+    rows = S.sweep(_sweep_builder, S.SweepRequest([20, 13, 20], [2.0, 1.0], "kc",
+                                                 onCell=lambda r, d, t: seen.append((d, t))))
+    assert [(r.nConn, r.gScale) for r in rows] == [(13, 1.0), (13, 2.0), (20, 1.0), (20, 2.0)]
+    assert all(r.failed and r.sumNaNs == -1 and np.isnan(r.avgSpike) for r in rows)
+    assert "13" in rows[0].error and "device" in rows[2].error.lower()
+    assert seen == [(1, 4), (2, 4), (3, 4), (4, 4)]
