@@ -382,8 +382,9 @@ def main():
 
     # -- e2e through the public C ABI with host buffers (rank 0, 1 s per step).
     # Same scope as the reference arm (which times Simulation::step, not the
-    # constructor): per step, ssb_step(10,000) and the step's raster moved into
-    # host memory (ssb_raster_drain); wall clock.  The network is uploaded once
+    # constructor): ssb_step(10,000) per bench step with that step's raster
+    # moved into host memory (ssb_raster_drain_async hands it to the copier so
+    # the next step computes meanwhile; a final ssb_raster_drain waits); wall clock.  The network is uploaded once
     # at construction (like the reference, untimed) and the Poisson drive is
     # the model's own RNG stream advanced on the device (part of the step), so
     # no per-step host input exists: h2d_bytes_per_step = 0.  For reference,
@@ -391,22 +392,24 @@ def main():
     # ssb_finish of a fresh 1 s run.
     e2e = None
     if not args.no_e2e:
-        k_e2e = 3
+        k_e2e = 4
         spec_e = make_spec(k_e2e + 1.0, seed=11)
         sim_e = S.Simulation(spec_e, S.StorageMode.FromSpec,
                              S.EngineOptions(device=dev, window=args.window))
         sim_e.step(STEPS_PER_SIM_SECOND)
         held = sim_e.drain_raster()
-        vals, d2h = [], []
+        c0 = sim_e.spike_counts()
+        # each step's raster is handed to the background copier as soon as the
+        # step is done; the next step computes while it drains; the timed
+        # region ends when the last step's events are in host memory
+        t0 = time.perf_counter()
         for _ in range(k_e2e):
-            c0 = sim_e.spike_counts()
-            t0 = time.perf_counter()
             sim_e.step(STEPS_PER_SIM_SECOND)
-            n = sim_e.drain_raster()
-            t1 = time.perf_counter()
-            vals.append(synaptic_events(spec_e, sim_e.spike_counts() - c0) / (t1 - t0))
-            d2h.append(4 * (n - held))
-            held = n
+            sim_e.drain_raster(wait=False)
+        n = sim_e.drain_raster()
+        t1 = time.perf_counter()
+        vals = [synaptic_events(spec_e, sim_e.spike_counts() - c0) / (t1 - t0)]
+        d2h = [4 * (n - held) / k_e2e]
         sim_e.close()
         wb = []
         for i in range(2):
@@ -423,9 +426,11 @@ def main():
             sim1.close()
         e2e = {"value": statistics.median(vals), "unit": UNIT, "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": int(statistics.median(d2h)),
-               "what": "per bench step: ssb_step(10,000) + ssb_raster_drain (the step's raster "
-                       "events into host memory), wall clock, median of 3; network uploaded "
-                       "once at construction (untimed, as in the reference arm)",
+               "what": "4 bench steps of ssb_step(10,000), each step's raster events moved "
+                       "to host memory (ssb_raster_drain_async, overlapping the next step; "
+                       "the final ssb_raster_drain inside the timed region), wall clock; "
+                       "network uploaded once at construction (untimed, as in the "
+                       "reference arm)",
                "with_build": {"value": max(wb), "what": "ssb_create (host build + upload) + "
                               "10,000 steps + ssb_finish, wall clock, best of 2"}}
 

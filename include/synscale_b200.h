@@ -336,6 +336,10 @@ SSB_API int ssb_raster_discard(ssb_sim* sim);
  * host memory (the engine otherwise drains in the background); returns the
  * number of events held on the host in *n_events. */
 SSB_API int ssb_raster_drain(ssb_sim* sim, int64_t* n_events);
+/* Starts moving the events recorded so far to host memory in the background
+ * and returns at once (steps issued next overlap the copy); a later
+ * ssb_raster_drain or ssb_finish waits for it. */
+SSB_API int ssb_raster_drain_async(ssb_sim* sim);
 
 /* ---- introspection / measurement ------------------------------------------- */
 SSB_API void* ssb_stream(ssb_sim* sim); /* the handle's cudaStream_t */

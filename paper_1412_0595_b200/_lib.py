@@ -167,6 +167,7 @@ _SIGNATURES = {
     "ssb_spike_counts": (C.c_int, [_vp, P(_i64), _i32]),
     "ssb_raster_discard": (C.c_int, [_vp]),
     "ssb_raster_drain": (C.c_int, [_vp, P(_i64)]),
+    "ssb_raster_drain_async": (C.c_int, [_vp]),
     "ssb_stream": (_vp, [_vp]),
     "ssb_window": (_i32, [_vp]),
     "ssb_block_size": (_i32, [_vp, _i32]),

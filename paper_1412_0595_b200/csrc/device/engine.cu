@@ -1579,9 +1579,15 @@ void DeviceEngine::collect_raster(std::vector<std::int32_t>& counts,
     }
 }
 
-std::int64_t DeviceEngine::drain_raster() {
+std::int64_t DeviceEngine::drain_raster(bool wait) {
     auto& m = *impl_;
     CK(cudaSetDevice(m.cfg.device));
+    if (!wait) {
+        // hand the events recorded so far to the background copier and
+        // return: the steps enqueued next overlap the device-to-host copy
+        if (!m.rasterDiscarded) m.flush_raster(false);
+        return -1;
+    }
     if (!m.rasterDiscarded) m.flush_raster(true);
     m.join_copier();
     std::int64_t n = 0;

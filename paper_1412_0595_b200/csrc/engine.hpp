@@ -153,7 +153,10 @@ public:
     // (step, pop, neuron) order.
     void collect_raster(std::vector<std::int32_t>& counts, std::vector<std::int32_t>& neurons);
     void discard_raster();
-    std::int64_t drain_raster();  // synchronous flush to the host store; events held
+    // Flush of the recorded events to the host store: wait = true returns the
+    // events held once everything is on the host; wait = false starts the copy
+    // in the background and returns -1.
+    std::int64_t drain_raster(bool wait = true);
     void spike_totals(std::vector<std::int64_t>& perPop);
 
     // Neurons of population pop held by this process: [lo, lo + n) of

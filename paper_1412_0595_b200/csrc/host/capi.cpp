@@ -830,6 +830,10 @@ int ssb_raster_drain(ssb_sim* sim, int64_t* n_events) {
     });
 }
 
+int ssb_raster_drain_async(ssb_sim* sim) {
+    return on_sim(sim, [&](ssb::SimCore& c) { c.engine().drain_raster(false); });
+}
+
 int ssb_raster_discard(ssb_sim* sim) {
     return on_sim(sim, [&](ssb::SimCore& c) { c.engine().discard_raster(); });
 }

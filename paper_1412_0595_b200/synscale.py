@@ -609,9 +609,13 @@ class Simulation:
     def discard_raster(self) -> None:
         self._check(lib.ssb_raster_discard(self._h))
 
-    def drain_raster(self) -> int:
-        """Waits for the issued steps and moves every recorded event to host
-        memory; returns the number of events now held on the host."""
+    def drain_raster(self, wait: bool = True) -> int:
+        """Moves every recorded event to host memory.  wait=True returns the
+        number of events held on the host once they are there; wait=False starts
+        the copy in the background (steps issued next overlap it), returns -1."""
+        if not wait:
+            self._check(lib.ssb_raster_drain_async(self._h))
+            return -1
         n = C.c_int64()
         self._check(lib.ssb_raster_drain(self._h, C.byref(n)))
         return n.value
