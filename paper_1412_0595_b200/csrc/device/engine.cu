@@ -407,6 +407,7 @@ struct DeviceEngine::Impl {
     // streams so they never compete for SMs; narrow ones overlap them freely.
     bool multiStream = false;
     cudaEvent_t lastWide = nullptr;
+    cudaEvent_t lastCollective = nullptr;  // the previous NCCL call of this enqueue
     bool is_wide(long long blocks, int smem) const {
         return blocks >= smCount / 4 && smem >= 32 * 1024;
     }
@@ -1037,9 +1038,18 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
     }
     if (P.sharded) {
         // the window's exchange: every rank's local bits, in rank order
-        if (comm)
+        if (comm) {
+            // collectives of one communicator must run in the same order on
+            // every rank: chain them (the enqueue order is identical on all
+            // ranks; independent streams could otherwise reorder them)
+            if (multiStream && lastCollective) CK(cudaStreamWaitEvent(sp, lastCollective, 0));
             comm->allgather_u32(P.kdev[b].bits, P.gathered[b],
                                 static_cast<std::size_t>(W) * P.nwords, sp);
+            if (multiStream) {
+                lastCollective = capture_event();
+                CK(cudaEventRecord(lastCollective, sp));
+            }
+        }
         if (!virtualShard) assemble_compact(pi, W, b, sp);  // virtual: after the shard copies
     }
 }
@@ -1106,6 +1116,7 @@ void DeviceEngine::Impl::enqueue_windows(int W, int M) {
     evUsed = 0;
     multiStream = multi;
     lastWide = nullptr;
+    lastCollective = nullptr;
     auto mark = [&](int sidx) -> cudaEvent_t {
         if (!multi) return nullptr;
         cudaEvent_t e = capture_event();
