@@ -1284,7 +1284,10 @@ DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfgIn)
     if (!virt && R > 1 && (cfg.rank < 0 || cfg.rank >= R))
         throw synscale::SpecError("rank " + std::to_string(cfg.rank) + " outside a world of " +
                                   std::to_string(R));
-    const ShardPlan plan = R > 1 ? plan_shards(net, R, cfg.shardMinSize) : ShardPlan{};
+    // a communicator id with a world of one rank still runs the split path
+    // (exchange included) on a one-rank communicator
+    const bool split = R > 1 || (!virt && cfg.hasCommId);
+    const ShardPlan plan = split ? plan_shards(net, R, cfg.shardMinSize, true) : ShardPlan{};
     const int smCount = device_props(cfg.device).smCount;
     auto init = [&](Impl& m, int rank, cudaStream_t shared) {
         m.cfg = cfg;
@@ -1304,9 +1307,9 @@ DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfgIn)
         }
         try {
             ShardStore store;
-            const HostNet local = R > 1 ? shard_net(net, plan, rank, store) : HostNet{};
-            if (R > 1 && !virt) m.comm = std::make_unique<Comm>(R, rank, cfg.commId.data());
-            m.build(R > 1 ? local : net);
+            const HostNet local = split ? shard_net(net, plan, rank, store) : HostNet{};
+            if (split && !virt) m.comm = std::make_unique<Comm>(R, rank, cfg.commId.data());
+            m.build(split ? local : net);
         } catch (...) {
             m.release();
             throw;

@@ -94,7 +94,9 @@ struct ShardPlan {
     std::vector<int> chunk;  // bounds[p][r] = min(r * chunk[p], n)
     bool split(int p) const { return !bounds[p].empty(); }
 };
-ShardPlan plan_shards(const HostNet& net, int world, int minSize);
+// force: split even a world of one rank (a one-rank NCCL communicator runs
+// the whole exchange path; used to test it on one GPU)
+ShardPlan plan_shards(const HostNet& net, int world, int minSize, bool force = false);
 
 // Matrices owned by a rank's local network (column slices).
 struct ShardStore {

@@ -21,13 +21,13 @@ namespace {
 int round_up(int v, int u) { return (v + u - 1) / u * u; }
 }  // namespace
 
-ShardPlan plan_shards(const HostNet& net, int world, int minSize) {
+ShardPlan plan_shards(const HostNet& net, int world, int minSize, bool force) {
     ShardPlan plan;
     plan.world = std::max(1, world);
     const int np = static_cast<int>(net.pops.size());
     plan.bounds.assign(np, {});
     plan.chunk.assign(np, 0);
-    if (plan.world == 1) return plan;
+    if (plan.world == 1 && !force) return plan;
     // feed-forward check (the windowed schedule exchanges once per window)
     std::vector<std::vector<int>> succ(np);
     std::vector<int> indeg(np, 0);
@@ -64,7 +64,9 @@ ShardPlan plan_shards(const HostNet& net, int world, int minSize) {
 
 HostNet shard_net(const HostNet& net, const ShardPlan& plan, int rank, ShardStore& store) {
     HostNet out = net;
-    if (plan.world <= 1) return out;
+    bool any = false;
+    for (const auto& b : plan.bounds) any = any || !b.empty();
+    if (!any) return out;
     if (rank < 0 || rank >= plan.world)
         throw synscale::SpecError("rank " + std::to_string(rank) + " outside a world of " +
                                   std::to_string(plan.world));

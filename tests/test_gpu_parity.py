@@ -477,3 +477,22 @@ def test_sweep_cells_match_oracle(oracle_mod):
         assert r.avgSpike == float(o.rates()[kc]), (r.nConn, r.gScale)
         assert r.sumNaNs == o.sum_nans()
     assert len({r.avgSpike for r in rows}) > 1
+
+
+@pytest.mark.parametrize("name", ["cfg3_20ms", "cfg2_100ms", "izh_ff_200ms"])
+def test_nccl_split_path_one_rank_matches_golden(golden, name):
+    """A communicator id with a world of one rank runs the whole split path on
+    a real (one-rank) NCCL communicator: per-window all-gathers captured in the
+    window graphs, assembly, compaction, gathered state pulls and the NaN sum."""
+    spec, mode = GOLDEN[name]()
+    g = golden["runs"][name]
+    sim = gpu_sim(spec, mode, window=64, world=1, rank=0, commId=S.comm_unique_id(),
+                  shardMinSize=32)
+    r = sim.finish()
+    assert specs.sha(r.raster.step, r.raster.population, r.raster.neuron) == g["raster_sha"]
+    assert r.sumNaNs == g["sum_nans"]
+    for pi, p in enumerate(spec.populations):
+        for f, h in g["state_sha"][p.name].items():
+            if p.model == S.ModelKind.PoissonSource and f in ("v", "gExc", "gInh"):
+                continue
+            assert specs.sha(sim.pull(pi, f)) == h, (p.name, f)
