@@ -153,7 +153,7 @@ CrsMatrix scale(const CrsMatrix& m, double gScale);
 
 // ---- network model (reference network.hpp:12-144) --------------------------
 
-enum class ModelKind { Izhikevich, PoissonSource, CondLif };
+enum class ModelKind { Izhikevich, PoissonSource, CondLif, TraubMiles };
 enum class SynapseSign { Excitatory, Inhibitory };
 enum class StorageKind { Dense, Sparse };
 
@@ -177,12 +177,31 @@ struct CondLifParams {
     double tauSynMs = 5.0;
 };
 
+// B200 extension (not in the reference): the Traub-Miles
+// Hodgkin-Huxley neuron of the paper's mushroom-body KCs (GeNN's TraubMiles:
+// Na / K / leak currents, `substeps` explicit-Euler sub-steps of dt/substeps
+// per step, spike on the upward crossing of 0 mV) with the same conductance
+// synapses as CondLif (decay exp(-dt/tauSyn), reversal eExc / eInh).
+struct TraubMilesParams {
+    double gNa = 7.15;     // uS
+    double ENa = 50.0;     // mV
+    double gK = 1.43;
+    double EK = -95.0;
+    double gl = 0.02672;
+    double El = -63.563;
+    double C = 0.143;      // nF
+    double eExcMV = 0.0;
+    double eInhMV = -92.0;
+    double tauSynMs = 3.0;
+    std::int32_t substeps = 25;
+};
+
 struct NeuronPopulation {
     std::string name;
     std::int32_t size = 0;
     ModelKind model = ModelKind::Izhikevich;
     std::uint64_t seed = 0;
-    std::variant<IzhikevichParams, PoissonParams, CondLifParams> params;
+    std::variant<IzhikevichParams, PoissonParams, CondLifParams, TraubMilesParams> params;
 };
 
 struct SynapseGroupSpec {
@@ -242,6 +261,9 @@ struct MBodyBuildOptions {
     double pnLhiWeight = 0.02;
     double lhiKcWeight = 0.01;
     double kcDnWeight = 0.01;
+    // extension: the KC model (CondLif as the reference, or Traub-Miles HH)
+    ModelKind kcModel = ModelKind::CondLif;
+    TraubMilesParams kcHH{};
 };
 
 NetworkSpec build_mbody_net(std::int32_t nPN, std::int32_t nLHI, std::int32_t nKC, std::int32_t nDN,
@@ -284,6 +306,7 @@ struct PopulationState {
     std::vector<scalar> excIn, inhIn;
     std::vector<std::uint8_t> nanFlag;
     std::int64_t flagged = 0;
+    std::vector<scalar> m, h, n;  // Traub-Miles gating variables (extension)
 };
 
 // Both run on the GPU over the caller's host arrays (no CPU path).

@@ -47,7 +47,8 @@ extern "C" {
 #define SSB_ERR_SPEC 2
 
 /* ModelKind (network.hpp:14) */
-enum { SSB_MODEL_IZHIKEVICH = 0, SSB_MODEL_POISSON = 1, SSB_MODEL_CONDLIF = 2 };
+enum { SSB_MODEL_IZHIKEVICH = 0, SSB_MODEL_POISSON = 1, SSB_MODEL_CONDLIF = 2,
+       SSB_MODEL_TRAUBMILES = 3 /* extension: Traub-Miles HH (F1) */ };
 /* SynapseSign (network.hpp:15) */
 enum { SSB_SIGN_EXC = 0, SSB_SIGN_INH = 1 };
 /* StorageKind (network.hpp:16) */
@@ -65,7 +66,10 @@ enum {
     SSB_FIELD_EXCIN = 4,   /* float[n]   accumulator for the next step */
     SSB_FIELD_INHIN = 5,   /* float[n]   accumulator for the next step */
     SSB_FIELD_NANFLAG = 6, /* uint8[n]   sticky non-finite flag */
-    SSB_FIELD_FLAGGED = 7  /* int64[1]   neurons ever flagged */
+    SSB_FIELD_FLAGGED = 7, /* int64[1]   neurons ever flagged */
+    SSB_FIELD_M = 8,       /* float[n]   Traub-Miles gating variables (extension) */
+    SSB_FIELD_H = 9,
+    SSB_FIELD_N = 10
 };
 
 /* NeuronPopulation (network.hpp:47-53) with its parameter variant flattened. */
@@ -80,6 +84,10 @@ typedef struct ssb_pop_desc {
     double tau_m_ms, e_leak_mv, v_thresh_mv, v_reset_mv, e_exc_mv, e_inh_mv, tau_syn_ms;
     /* IzhikevichParams (network.hpp:21-26): per-neuron arrays of `size` doubles */
     const double *izh_a, *izh_b, *izh_c, *izh_d, *izh_noise, *izh_bias;
+    /* TraubMilesParams (extension, F1); the synapses use e_exc_mv, e_inh_mv and
+     * tau_syn_ms above */
+    double hh_gna, hh_ena, hh_gk, hh_ek, hh_gl, hh_el, hh_c;
+    int32_t hh_substeps;
 } ssb_pop_desc;
 
 /* SynapseGroupSpec (network.hpp:59-70) with WeightDist (matrix.hpp:14-24). */
@@ -113,6 +121,11 @@ typedef struct ssb_mbody_opts {
     double dt_ms, duration_ms, pn_rate_hz, pn_kc_out_fraction;
     double tau_m_ms, e_leak_mv, v_thresh_mv, v_reset_mv, e_exc_mv, e_inh_mv, tau_syn_ms;
     double pn_kc_weight_hi, pn_lhi_weight, lhi_kc_weight, kc_dn_weight;
+    /* extension: KC model (SSB_MODEL_CONDLIF or SSB_MODEL_TRAUBMILES) and the HH
+     * parameters (synapses: e_exc_mv / e_inh_mv above, kc_tau_syn_ms) */
+    int32_t kc_model;
+    double hh_gna, hh_ena, hh_gk, hh_ek, hh_gl, hh_el, hh_c, hh_e_inh_mv, kc_tau_syn_ms;
+    int32_t hh_substeps;
 } ssb_mbody_opts;
 
 /* IzhBuildOptions (network.hpp:105-114). */

@@ -196,6 +196,11 @@ typedef struct {
     double *noise, *bias;
     float tauM, eLeak, eExc, eInh, vThresh, vReset, synDecay;
     double p;
+    /* Traub-Miles (extension, F1; no reference implementation) */
+    float *hm, *hh, *hn;
+    uint8_t* above0; /* V >= 0 at the start of the current step */
+    float gNa, ENa, gK, EK, gl, El, Cm, mdt;
+    int substeps;
 } or_pop;
 
 typedef struct {
@@ -283,6 +288,30 @@ OR_API or_sim* or_create(const ssb_net_desc* net, int mode, char* err, size_t er
             }
             snprintf(label, sizeof label, "%s/noise", d->name);
             or_stream_init(&p->rng, net->global_seed, d->seed, label);
+        } else if (d->model == SSB_MODEL_TRAUBMILES) {
+            /* extension (F1): fp32 constants, GeNN TraubMiles initial state */
+            p->gNa = (float)d->hh_gna;
+            p->ENa = (float)d->hh_ena;
+            p->gK = (float)d->hh_gk;
+            p->EK = (float)d->hh_ek;
+            p->gl = (float)d->hh_gl;
+            p->El = (float)d->hh_el;
+            p->Cm = (float)d->hh_c;
+            p->eExc = (float)d->e_exc_mv;
+            p->eInh = (float)d->e_inh_mv;
+            p->substeps = d->hh_substeps;
+            p->mdt = (float)(net->dt_ms / d->hh_substeps);
+            p->synDecay = (float)exp(-net->dt_ms / d->tau_syn_ms);
+            p->hm = zalloc_f(n);
+            p->hh = zalloc_f(n);
+            p->hn = zalloc_f(n);
+            p->above0 = (uint8_t*)calloc(n ? n : 1, 1);
+            for (size_t i = 0; i < n; ++i) {
+                p->v[i] = -60.0f;
+                p->hm[i] = 0.0529324f;
+                p->hh[i] = 0.3176767f;
+                p->hn[i] = 0.5961207f;
+            }
         } else if (d->model == SSB_MODEL_POISSON) {
             p->p = d->rate_hz * net->dt_ms / 1000.0; /* engine.cpp:186 */
             snprintf(label, sizeof label, "%s/source", d->name);
@@ -376,6 +405,7 @@ OR_API void or_destroy(or_sim* s) {
     for (int i = 0; i < s->npops; ++i) {
         or_pop* p = &s->pops[i];
         free(p->v), free(p->u), free(p->gExc), free(p->gInh), free(p->excIn), free(p->inhIn);
+        free(p->hm), free(p->hh), free(p->hn), free(p->above0);
         free(p->nanFlag), free(p->spikes), free(p->a), free(p->b), free(p->c), free(p->d);
         free(p->noise), free(p->bias);
     }
@@ -387,6 +417,66 @@ OR_API void or_destroy(or_sim* s) {
     free(s);
 }
 
+/* ---- Traub-Miles HH (extension) ----------------------
+ * Not in the reference: GeNN's TraubMiles neuron (the model of the paper's
+ * mushroom-body KCs) with CondLif-style conductance synapses.  This is the
+ * definition the device kernel follows operation for operation (kernels.cuh
+ * hh_step / hh_expf); its parity is against this restatement only. */
+static float or_hh_expf(float x) {
+    if (!(x > -87.0f)) return x != x ? x : 0.0f;
+    if (x > 88.0f) return INFINITY;
+    const float kf = rintf(x * 1.44269504089f);
+    float r = fmaf(-kf, 0.693145751953125f, x);
+    r = fmaf(-kf, 1.428606765330187e-06f, r);
+    float q = 1.98412698e-4f;
+    q = fmaf(q, r, 1.38888889e-3f);
+    q = fmaf(q, r, 8.33333333e-3f);
+    q = fmaf(q, r, 4.16666667e-2f);
+    q = fmaf(q, r, 1.66666667e-1f);
+    q = fmaf(q, r, 0.5f);
+    q = fmaf(q, r, 1.0f);
+    q = fmaf(q, r, 1.0f);
+    return ldexpf(q, (int)kf);
+}
+
+static float or_hh_ratio(float k, float num, float den) {
+    return (k * num) / (or_hh_expf(num / den) - 1.0f);
+}
+
+static void or_hh_advance(or_pop* p) {
+    for (int i = 0; i < p->n; ++i) {
+        const float ge = p->gExc[i] * p->synDecay + p->excIn[i];
+        const float gi = p->gInh[i] * p->synDecay - p->inhIn[i];
+        float V = p->v[i], m = p->hm[i], h = p->hh[i], n = p->hn[i];
+        const float isyn = ge * (p->eExc - V) + gi * (p->eInh - V);
+        p->above0[i] = V >= 0.0f;
+        for (int st = 0; st < p->substeps; ++st) {
+            const float m3h = ((m * m) * m) * h;
+            const float n4 = ((n * n) * n) * n;
+            const float ina = (m3h * p->gNa) * (V - p->ENa);
+            const float ik = (n4 * p->gK) * (V - p->EK);
+            const float il = p->gl * (V - p->El);
+            const float imem = -(((ina + ik) + il) - isyn);
+            const float am = V == -52.0f ? 1.28f : or_hh_ratio(0.32f, -52.0f - V, 4.0f);
+            const float bm = V == -25.0f ? 1.4f : or_hh_ratio(0.28f, V + 25.0f, 5.0f);
+            const float ah = 0.128f * or_hh_expf((-48.0f - V) / 18.0f);
+            const float bh = 4.0f / (or_hh_expf((-25.0f - V) / 5.0f) + 1.0f);
+            const float an = V == -50.0f ? 0.16f : or_hh_ratio(0.032f, -50.0f - V, 5.0f);
+            const float bn = 0.5f * or_hh_expf((-55.0f - V) / 40.0f);
+            m = m + ((am * (1.0f - m)) - (bm * m)) * p->mdt;
+            h = h + ((ah * (1.0f - h)) - (bh * h)) * p->mdt;
+            n = n + ((an * (1.0f - n)) - (bn * n)) * p->mdt;
+            V = V + (imem / p->Cm) * p->mdt;
+        }
+        p->gExc[i] = ge;
+        p->gInh[i] = gi;
+        p->v[i] = V;
+        p->hm[i] = m;
+        p->hh[i] = h;
+        p->hn[i] = n;
+    }
+}
+
 /* detect_nans (engine.cpp:27-51) */
 static int64_t or_detect_nans_impl(int kind, const float* v, const float* u, const float* ge,
                                    const float* gi, uint8_t* flag, int64_t n) {
@@ -396,7 +486,7 @@ static int64_t or_detect_nans_impl(int kind, const float* v, const float* u, con
         int bad = 0;
         if (kind == SSB_MODEL_IZHIKEVICH)
             bad = !isfinite(v[i]) || !isfinite(u[i]);
-        else if (kind == SSB_MODEL_CONDLIF)
+        else if (kind == SSB_MODEL_CONDLIF || kind == SSB_MODEL_TRAUBMILES)
             bad = !isfinite(v[i]) || !isfinite(ge[i]) || !isfinite(gi[i]);
         if (bad) {
             flag[i] = 1;
@@ -421,6 +511,8 @@ static void or_advance(or_sim* s, or_pop* p) {
             p->v[i] = v;
             p->u[i] = u;
         }
+    } else if (p->kind == SSB_MODEL_TRAUBMILES) {
+        or_hh_advance(p);
     } else if (p->kind == SSB_MODEL_CONDLIF) {
         for (int i = 0; i < p->n; ++i) {
             const float ge = p->gExc[i] * p->synDecay + p->excIn[i];
@@ -452,6 +544,10 @@ static void or_threshold(or_pop* p) {
                 p->spikes[p->nspk++] = i;
                 p->v[i] = p->vReset;
             }
+    } else if (p->kind == SSB_MODEL_TRAUBMILES) {
+        /* upward crossing of 0 mV, no reset (GeNN TraubMiles) */
+        for (int i = 0; i < p->n; ++i)
+            if (p->v[i] >= 0.0f && !p->above0[i]) p->spikes[p->nspk++] = i;
     }
 }
 
@@ -559,6 +655,9 @@ static void* or_field(or_sim* s, int pop, int field, size_t* esz) {
     case SSB_FIELD_EXCIN: return p->excIn;
     case SSB_FIELD_INHIN: return p->inhIn;
     case SSB_FIELD_NANFLAG: *esz = 1; return p->nanFlag;
+    case SSB_FIELD_M: return p->hm;
+    case SSB_FIELD_H: return p->hh;
+    case SSB_FIELD_N: return p->hn;
     }
     return NULL;
 }

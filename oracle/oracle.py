@@ -22,6 +22,7 @@ REF_LIB = os.path.join(HERE, "_ref", "libsynscale_ref.so")
 REF_SRC = "/root/reference/proj"
 
 FIELD_IDS = {"v": 0, "u": 1, "gExc": 2, "gInh": 3, "excIn": 4, "inhIn": 5, "nanFlag": 6,
+             "m": 8, "h": 9, "n": 10,
              "flagged": 7}
 
 

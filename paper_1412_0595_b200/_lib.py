@@ -14,13 +14,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsynscale_b200.so")
 
 SSB_OK, SSB_ERR_INTERNAL, SSB_ERR_SPEC = 0, 1, 2
-MODEL_IZHIKEVICH, MODEL_POISSON, MODEL_CONDLIF = 0, 1, 2
+MODEL_IZHIKEVICH, MODEL_POISSON, MODEL_CONDLIF, MODEL_TRAUBMILES = 0, 1, 2, 3
 SIGN_EXC, SIGN_INH = 0, 1
 STORAGE_DENSE, STORAGE_SPARSE = 0, 1
 MODE_FROM_SPEC, MODE_FORCE_DENSE, MODE_FORCE_SPARSE = 0, 1, 2
 WEIGHT_CONSTANT, WEIGHT_UNIFORM = 0, 1
 (FIELD_V, FIELD_U, FIELD_GEXC, FIELD_GINH, FIELD_EXCIN, FIELD_INHIN, FIELD_NANFLAG,
- FIELD_FLAGGED) = range(8)
+ FIELD_FLAGGED, FIELD_M, FIELD_H, FIELD_N) = range(11)
 
 
 class ssb_pop_desc(C.Structure):
@@ -33,6 +33,9 @@ class ssb_pop_desc(C.Structure):
         ("izh_a", C.POINTER(C.c_double)), ("izh_b", C.POINTER(C.c_double)),
         ("izh_c", C.POINTER(C.c_double)), ("izh_d", C.POINTER(C.c_double)),
         ("izh_noise", C.POINTER(C.c_double)), ("izh_bias", C.POINTER(C.c_double)),
+        ("hh_gna", C.c_double), ("hh_ena", C.c_double), ("hh_gk", C.c_double),
+        ("hh_ek", C.c_double), ("hh_gl", C.c_double), ("hh_el", C.c_double),
+        ("hh_c", C.c_double), ("hh_substeps", C.c_int32),
     ]
 
 
@@ -58,7 +61,9 @@ class ssb_mbody_opts(C.Structure):
     _fields_ = [(n, C.c_double) for n in (
         "dt_ms", "duration_ms", "pn_rate_hz", "pn_kc_out_fraction", "tau_m_ms", "e_leak_mv",
         "v_thresh_mv", "v_reset_mv", "e_exc_mv", "e_inh_mv", "tau_syn_ms", "pn_kc_weight_hi",
-        "pn_lhi_weight", "lhi_kc_weight", "kc_dn_weight")]
+        "pn_lhi_weight", "lhi_kc_weight", "kc_dn_weight")] + [("kc_model", C.c_int32)] + [
+        (n, C.c_double) for n in ("hh_gna", "hh_ena", "hh_gk", "hh_ek", "hh_gl", "hh_el", "hh_c",
+                                  "hh_e_inh_mv", "kc_tau_syn_ms")] + [("hh_substeps", C.c_int32)]
 
 
 class ssb_izh_opts(C.Structure):

@@ -157,6 +157,7 @@ bool kernel_attributes(const std::string& name, int& regs, int& sharedBytes, int
     cudaError_t e;
     if (name == "condlif_window") e = cudaFuncGetAttributes(&a, ssbk::condlif_window_kernel);
     else if (name == "izh_window") e = cudaFuncGetAttributes(&a, ssbk::izh_window_kernel);
+    else if (name == "hh_window") e = cudaFuncGetAttributes(&a, ssbk::hh_window_kernel);
     else if (name == "gaussian_window") e = cudaFuncGetAttributes(&a, ssbk::gaussian_window_kernel);
     else if (name == "poisson_window") e = cudaFuncGetAttributes(&a, ssbk::poisson_window_kernel);
     else if (name == "dense_window") e = cudaFuncGetAttributes(&a, ssbk::dense_window_kernel);
@@ -689,7 +690,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
                 for (int gi : gl)
                     if (!net.groups[gi].dense) P.sparseInline = true;
         }
-        if (hp.kind == kCondLif || hp.kind == kIzhikevich) {
+        if (hp.kind == kCondLif || hp.kind == kIzhikevich || hp.kind == kTraubMiles) {
             // tile size from the occupancy model (registers of the kernel +
             // this tile's shared-memory plan, 1 KB per-block reservation)
             ssbk::StageAcc tmp[2];
@@ -699,9 +700,9 @@ void DeviceEngine::Impl::build(const HostNet& net) {
                 [&](int tn) {
                     return plan_stage(net, pi, tn, tmp, tmpIn, tmpC, tmpBits) + 1024;
                 },
-                hp.kind == kIzhikevich
-                    ? reinterpret_cast<const void*>(&ssbk::izh_window_kernel)
-                    : reinterpret_cast<const void*>(&ssbk::condlif_window_kernel));
+                hp.kind == kIzhikevich   ? reinterpret_cast<const void*>(&ssbk::izh_window_kernel)
+                : hp.kind == kTraubMiles ? reinterpret_cast<const void*>(&ssbk::hh_window_kernel)
+                                         : reinterpret_cast<const void*>(&ssbk::condlif_window_kernel));
             P.grid = (hp.n + P.tileN - 1) / P.tileN;
             // a single-block population gets extra threads for the parallel phases
             P.block = P.grid == 1 ? P.tileN * std::max(1, 256 / P.tileN) : P.tileN;
@@ -768,6 +769,28 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         if (hp.kind == kCondLif) {
             std::vector<float> v0(n, hp.eLeak);  // engine.cpp:199
             CK(cudaMemcpyAsync(d.v, v0.data(), n * sizeof(float), cudaMemcpyHostToDevice, stream));
+            CK(cudaStreamSynchronize(stream));
+        }
+        if (hp.kind == kTraubMiles) {
+            // extension (F1): GeNN TraubMiles initial state
+            std::vector<float> v0(n, -60.0f), m0(n, 0.0529324f), h0(n, 0.3176767f),
+                n0(n, 0.5961207f);
+            d.hm = alloc<float>(n);
+            d.hh = alloc<float>(n);
+            d.hn = alloc<float>(n);
+            CK(cudaMemcpyAsync(d.v, v0.data(), n * 4, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(d.hm, m0.data(), n * 4, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(d.hh, h0.data(), n * 4, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(d.hn, n0.data(), n * 4, cudaMemcpyHostToDevice, stream));
+            d.gNa = hp.gNa;
+            d.ENa = hp.ENa;
+            d.gK = hp.gK;
+            d.EK = hp.EK;
+            d.gl = hp.gl;
+            d.El = hp.El;
+            d.Cm = hp.Cm;
+            d.mdt = hp.mdt;
+            d.substeps = hp.substeps;
             CK(cudaStreamSynchronize(stream));
         }
         if (hp.kind == kIzhikevich) {
@@ -954,6 +977,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     };
     allow(reinterpret_cast<const void*>(&ssbk::condlif_window_kernel), std::max(maxSmem, 4096));
     allow(reinterpret_cast<const void*>(&ssbk::izh_window_kernel), std::max(maxSmem, 4096));
+    allow(reinterpret_cast<const void*>(&ssbk::hh_window_kernel), std::max(maxSmem, 4096));
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_warp_kernel), kWarpRingBytes);
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_pipe_kernel), ring_smem());
     if (const char* e = std::getenv("SSB_DENSE_KERNEL")) usePipe = std::string(e) == "pipe";
@@ -1012,6 +1036,12 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
             });
             launch("izh_window:" + P.name, [&] {
                 ssbk::izh_window_kernel<<<P.grid, P.block, P.smemBytes, sm>>>(
+                    K, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk,
+                    P.offIn, P.offBits);
+            });
+        } else if (P.kind == kTraubMiles) {
+            launch("hh_window:" + P.name, [&] {
+                ssbk::hh_window_kernel<<<P.grid, P.block, P.smemBytes, sm>>>(
                     K, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk,
                     P.offIn, P.offBits);
             });
@@ -1456,6 +1486,9 @@ void* field_ptr(const ssbk::PopDev& d, int field, std::size_t& esz) {
     case kFieldExcIn: return d.excIn;
     case kFieldInhIn: return d.inhIn;
     case kFieldNanFlag: esz = 1; return d.nanFlag;
+    case kFieldM: return d.hm;
+    case kFieldH: return d.hh;
+    case kFieldN: return d.hn;
     case kFieldFlagged: esz = 8; return d.flagged;
     }
     return nullptr;

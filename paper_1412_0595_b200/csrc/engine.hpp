@@ -12,7 +12,7 @@
 
 namespace ssb {
 
-enum PopKind : int { kIzhikevich = 0, kPoisson = 1, kCondLif = 2 };
+enum PopKind : int { kIzhikevich = 0, kPoisson = 1, kCondLif = 2, kTraubMiles = 3 };
 
 // One population, compiled for the device: constants already cast to the
 // storage precision exactly as Simulation's constructor does
@@ -28,6 +28,9 @@ struct HostPop {
     // Izhikevich per-neuron parameters (fp32) and drives (fp64)
     std::vector<float> a, b, c, d;
     std::vector<double> noise, bias;
+    // Traub-Miles (extension): conductances fp32, sub-step length dt/substeps
+    float gNa = 0, ENa = 0, gK = 0, EK = 0, gl = 0, El = 0, Cm = 0, mdt = 0;
+    int substeps = 0;
     // RNG stream ("<name>/source" or "<name>/noise"): MT19937-64 state
     std::array<std::uint64_t, 312> mt{};
     int mtPos = 312;
@@ -126,7 +129,7 @@ struct KernelStat {
 
 enum StateField : int {
     kFieldV = 0, kFieldU, kFieldGExc, kFieldGInh, kFieldExcIn, kFieldInhIn, kFieldNanFlag,
-    kFieldFlagged
+    kFieldFlagged, kFieldM, kFieldH, kFieldN
 };
 
 // Thrown for CUDA failures (maps to SSB_ERR_INTERNAL).

@@ -82,6 +82,23 @@ NetworkSpec to_spec(const ssb_net_desc* d) {
             np.params = c;
             break;
         }
+        case SSB_MODEL_TRAUBMILES: {
+            np.model = ModelKind::TraubMiles;
+            TraubMilesParams h;
+            h.gNa = p.hh_gna;
+            h.ENa = p.hh_ena;
+            h.gK = p.hh_gk;
+            h.EK = p.hh_ek;
+            h.gl = p.hh_gl;
+            h.El = p.hh_el;
+            h.C = p.hh_c;
+            h.eExcMV = p.e_exc_mv;
+            h.eInhMV = p.e_inh_mv;
+            h.tauSynMs = p.tau_syn_ms;
+            h.substeps = p.hh_substeps;
+            np.params = h;
+            break;
+        }
         case SSB_MODEL_IZHIKEVICH: {
             np.model = ModelKind::Izhikevich;
             IzhikevichParams z;
@@ -156,6 +173,20 @@ ssb_net_desc* to_desc(const NetworkSpec& spec) {
             d.e_exc_mv = c.eExcMV;
             d.e_inh_mv = c.eInhMV;
             d.tau_syn_ms = c.tauSynMs;
+        } else if (p.model == ModelKind::TraubMiles) {
+            d.model = SSB_MODEL_TRAUBMILES;
+            const auto& h = std::get<TraubMilesParams>(p.params);
+            d.hh_gna = h.gNa;
+            d.hh_ena = h.ENa;
+            d.hh_gk = h.gK;
+            d.hh_ek = h.EK;
+            d.hh_gl = h.gl;
+            d.hh_el = h.El;
+            d.hh_c = h.C;
+            d.e_exc_mv = h.eExcMV;
+            d.e_inh_mv = h.eInhMV;
+            d.tau_syn_ms = h.tauSynMs;
+            d.hh_substeps = h.substeps;
         } else {
             d.model = SSB_MODEL_IZHIKEVICH;
             const auto& z = std::get<IzhikevichParams>(p.params);
@@ -225,7 +256,8 @@ ssb::HostNet skeleton(const NetworkSpec& spec) {
         ssb::HostPop hp;
         hp.name = p.name;
         hp.n = p.size;
-        hp.kind = p.model == ModelKind::CondLif ? ssb::kCondLif
+        hp.kind = p.model == ModelKind::TraubMiles ? ssb::kTraubMiles
+                  : p.model == ModelKind::CondLif ? ssb::kCondLif
                   : p.model == ModelKind::PoissonSource ? ssb::kPoisson
                                                          : ssb::kIzhikevich;
         net.pops.push_back(hp);
@@ -337,6 +369,22 @@ int ssb_build_mbody(int32_t n_pn, int32_t n_lhi, int32_t n_kc, int32_t n_dn,
             o.pnLhiWeight = opts->pn_lhi_weight;
             o.lhiKcWeight = opts->lhi_kc_weight;
             o.kcDnWeight = opts->kc_dn_weight;
+            if (opts->kc_model == SSB_MODEL_TRAUBMILES) {
+                o.kcModel = ModelKind::TraubMiles;
+                o.kcHH.gNa = opts->hh_gna;
+                o.kcHH.ENa = opts->hh_ena;
+                o.kcHH.gK = opts->hh_gk;
+                o.kcHH.EK = opts->hh_ek;
+                o.kcHH.gl = opts->hh_gl;
+                o.kcHH.El = opts->hh_el;
+                o.kcHH.C = opts->hh_c;
+                o.kcHH.eExcMV = opts->e_exc_mv;
+                o.kcHH.eInhMV = opts->hh_e_inh_mv;
+                o.kcHH.tauSynMs = opts->kc_tau_syn_ms;
+                o.kcHH.substeps = opts->hh_substeps;
+            } else if (opts->kc_model != SSB_MODEL_CONDLIF) {
+                throw SpecError("kc_model must be SSB_MODEL_CONDLIF or SSB_MODEL_TRAUBMILES");
+            }
         }
         std::map<std::string, double> gs;
         if (gscales) {
@@ -387,6 +435,17 @@ void ssb_mbody_default_opts(ssb_mbody_opts* o) {
     o->pn_lhi_weight = d.pnLhiWeight;
     o->lhi_kc_weight = d.lhiKcWeight;
     o->kc_dn_weight = d.kcDnWeight;
+    o->kc_model = SSB_MODEL_CONDLIF;
+    o->hh_gna = d.kcHH.gNa;
+    o->hh_ena = d.kcHH.ENa;
+    o->hh_gk = d.kcHH.gK;
+    o->hh_ek = d.kcHH.EK;
+    o->hh_gl = d.kcHH.gl;
+    o->hh_el = d.kcHH.El;
+    o->hh_c = d.kcHH.C;
+    o->hh_e_inh_mv = d.kcHH.eInhMV;
+    o->kc_tau_syn_ms = d.kcHH.tauSynMs;
+    o->hh_substeps = d.kcHH.substeps;
 }
 
 void ssb_izh_default_opts(ssb_izh_opts* o) {
@@ -692,7 +751,9 @@ int ssb_sync(ssb_sim* sim) {
 int ssb_pull_state(ssb_sim* sim, int32_t pop, int32_t field, void* dst, int64_t n) {
     return on_sim(sim, [&](ssb::SimCore& c) {
         if (pop < 0 || pop >= c.n_pops()) throw SpecError("population index out of range");
-        if (field < SSB_FIELD_V || field > SSB_FIELD_FLAGGED) throw SpecError("unknown state field");
+        if (field < SSB_FIELD_V || field > SSB_FIELD_N) throw SpecError("unknown state field");
+        if (field >= SSB_FIELD_M && c.pop_model(pop) != ModelKind::TraubMiles)
+            throw SpecError("gating variables m, h, n exist for Traub-Miles populations only");
         const int64_t want = field == SSB_FIELD_FLAGGED ? 1 : c.pop_size(pop);
         if (n != want)
             throw SpecError("state field holds " + std::to_string(want) + " elements, " +
@@ -705,7 +766,9 @@ int ssb_push_state(ssb_sim* sim, int32_t pop, int32_t field, const void* src, in
     return on_sim(sim, [&](ssb::SimCore& c) {
         if (c.finished()) throw SpecError("simulation already finished");
         if (pop < 0 || pop >= c.n_pops()) throw SpecError("population index out of range");
-        if (field < SSB_FIELD_V || field > SSB_FIELD_FLAGGED) throw SpecError("unknown state field");
+        if (field < SSB_FIELD_V || field > SSB_FIELD_N) throw SpecError("unknown state field");
+        if (field >= SSB_FIELD_M && c.pop_model(pop) != ModelKind::TraubMiles)
+            throw SpecError("gating variables m, h, n exist for Traub-Miles populations only");
         const int64_t want = field == SSB_FIELD_FLAGGED ? 1 : c.pop_size(pop);
         if (n != want)
             throw SpecError("state field holds " + std::to_string(want) + " elements, " +

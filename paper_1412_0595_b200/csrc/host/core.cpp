@@ -126,6 +126,23 @@ SimCore::SimCore(const NetworkSpec& spec, StorageMode mode, const EngineConfig& 
             p.synDecay = static_cast<scalar>(std::exp(-spec_.dtMs / c.tauSynMs));
             break;
         }
+        case ModelKind::TraubMiles: {  // extension (F1)
+            p.kind = kTraubMiles;
+            const auto& h = std::get<TraubMilesParams>(ps.params);
+            p.gNa = static_cast<scalar>(h.gNa);
+            p.ENa = static_cast<scalar>(h.ENa);
+            p.gK = static_cast<scalar>(h.gK);
+            p.EK = static_cast<scalar>(h.EK);
+            p.gl = static_cast<scalar>(h.gl);
+            p.El = static_cast<scalar>(h.El);
+            p.Cm = static_cast<scalar>(h.C);
+            p.eExc = static_cast<scalar>(h.eExcMV);
+            p.eInh = static_cast<scalar>(h.eInhMV);
+            p.substeps = h.substeps;
+            p.mdt = static_cast<scalar>(spec_.dtMs / h.substeps);
+            p.synDecay = static_cast<scalar>(std::exp(-spec_.dtMs / h.tauSynMs));
+            break;
+        }
         case ModelKind::Izhikevich: {
             p.kind = kIzhikevich;
             const auto& z = std::get<IzhikevichParams>(ps.params);

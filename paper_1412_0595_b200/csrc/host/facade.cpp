@@ -43,13 +43,19 @@ struct Simulation::Impl {
           observed(spec.populations.size(), 0),
           writable(spec.populations.size(), 0) {}
 
+    static constexpr int kMirrored[] = {ssb::kFieldV,     ssb::kFieldU,     ssb::kFieldGExc,
+                                        ssb::kFieldGInh,  ssb::kFieldExcIn, ssb::kFieldInhIn,
+                                        ssb::kFieldM,     ssb::kFieldH,     ssb::kFieldN};
     // fields a model keeps (the others stay empty, as in the reference)
     static bool uses(ModelKind m, int field) {
         switch (field) {
         case ssb::kFieldV: return m != ModelKind::PoissonSource;
         case ssb::kFieldU: return m == ModelKind::Izhikevich;
         case ssb::kFieldGExc:
-        case ssb::kFieldGInh: return m == ModelKind::CondLif;
+        case ssb::kFieldGInh: return m == ModelKind::CondLif || m == ModelKind::TraubMiles;
+        case ssb::kFieldM:
+        case ssb::kFieldH:
+        case ssb::kFieldN: return m == ModelKind::TraubMiles;
         default: return true;
         }
     }
@@ -61,6 +67,9 @@ struct Simulation::Impl {
         case ssb::kFieldGInh: return &s.gInh;
         case ssb::kFieldExcIn: return &s.excIn;
         case ssb::kFieldInhIn: return &s.inhIn;
+        case ssb::kFieldM: return &s.m;
+        case ssb::kFieldH: return &s.h;
+        case ssb::kFieldN: return &s.n;
         }
         return nullptr;
     }
@@ -70,7 +79,7 @@ struct Simulation::Impl {
         const ModelKind m = core.pop_model(p);
         const std::int64_t n = core.pop_size(p);
         auto& eng = const_cast<ssb::SimCore&>(core).engine();
-        for (int f = ssb::kFieldV; f <= ssb::kFieldInhIn; ++f) {
+        for (int f : kMirrored) {
             if (!uses(m, f)) continue;
             auto* v = vec(s, f);
             v->resize(static_cast<std::size_t>(n));
@@ -88,7 +97,7 @@ struct Simulation::Impl {
             const ModelKind m = core.pop_model(static_cast<int>(p));
             const std::int64_t n = core.pop_size(static_cast<int>(p));
             auto& eng = core.engine();
-            for (int f = ssb::kFieldV; f <= ssb::kFieldInhIn; ++f) {
+            for (int f : kMirrored) {
                 if (!uses(m, f)) continue;
                 auto* v = vec(s, f);
                 if (static_cast<std::int64_t>(v->size()) != n)

@@ -62,6 +62,22 @@ void check_izh(const NeuronPopulation& p, const IzhikevichParams& z, const std::
             }
 }
 
+// Traub-Miles (extension, F1): finite parameters, positive capacitance and
+// synaptic time constant, 1..1000 sub-steps.
+void check_hh(const TraubMilesParams& h, const std::string& at, Report& rep) {
+    const std::pair<double, const char*> fields[] = {
+        {h.gNa, "gNa"}, {h.ENa, "ENa"}, {h.gK, "gK"}, {h.EK, "EK"}, {h.gl, "gl"},
+        {h.El, "El"}, {h.C, "C"}, {h.eExcMV, "eExcMV"}, {h.eInhMV, "eInhMV"},
+        {h.tauSynMs, "tauSynMs"}};
+    for (const auto& [x, nm] : fields)
+        if (!fin(x)) rep.add(at + "." + nm, "must be finite");
+    if (fin(h.C) && !(h.C > 0.0)) rep.add(at + ".C", "membrane capacitance must be > 0");
+    if (fin(h.tauSynMs) && !(h.tauSynMs > 0.0))
+        rep.add(at + ".tauSynMs", "synaptic time constant must be > 0");
+    if (h.substeps < 1 || h.substeps > 1000)
+        rep.add(at + ".substeps", "substeps must lie in [1, 1000]");
+}
+
 void check_lif(const CondLifParams& c, const std::string& at, Report& rep) {
     const std::pair<double, const char*> fields[] = {
         {c.tauMMs, "tauMMs"}, {c.eLeakMV, "eLeakMV"}, {c.vThreshMV, "vThreshMV"},
@@ -116,7 +132,9 @@ std::vector<Violation> validate(const NetworkSpec& spec) {
                         (p.model == ModelKind::PoissonSource &&
                          std::holds_alternative<PoissonParams>(p.params)) ||
                         (p.model == ModelKind::CondLif &&
-                         std::holds_alternative<CondLifParams>(p.params));
+                         std::holds_alternative<CondLifParams>(p.params)) ||
+                        (p.model == ModelKind::TraubMiles &&
+                         std::holds_alternative<TraubMilesParams>(p.params));
         if (!ok) {
             rep.add(at + ".params", "the parameter block does not match the population model");
             continue;
@@ -128,6 +146,8 @@ std::vector<Violation> validate(const NetworkSpec& spec) {
             if (!fin(r) || r < 0.0) rep.add(at + ".params.rateHz", "rate must be finite and >= 0");
             else if (fin(spec.dtMs) && spec.dtMs > 0.0 && r * spec.dtMs / 1000.0 > 1.0)
                 rep.add(at + ".params.rateHz", "rate * dt gives a spike probability above 1");
+        } else if (p.model == ModelKind::TraubMiles) {
+            check_hh(std::get<TraubMilesParams>(p.params), at + ".params", rep);
         } else {
             check_lif(std::get<CondLifParams>(p.params), at + ".params", rep);
         }
@@ -298,6 +318,10 @@ NetworkSpec build_mbody_net(std::int32_t nPN, std::int32_t nLHI, std::int32_t nK
         p.model = ModelKind::CondLif;
         p.seed = entity++;
         p.params = opt.lif;
+        if (std::string(name) == "kc" && opt.kcModel == ModelKind::TraubMiles) {
+            p.model = ModelKind::TraubMiles;  // extension: HH KCs (F1)
+            p.params = opt.kcHH;
+        }
         spec.populations.push_back(std::move(p));
     }
     const auto kcFan =

@@ -50,7 +50,7 @@ ShardPlan plan_shards(const HostNet& net, int world, int minSize, bool force) {
     const int R = plan.world;
     for (int p = 0; p < np; ++p) {
         const auto& P = net.pops[p];
-        if (P.kind != kCondLif || P.n < std::max(minSize, R)) continue;
+        if ((P.kind != kCondLif && P.kind != kTraubMiles) || P.n < std::max(minSize, R)) continue;
         int chunk = (P.n + R - 1) / R;
         chunk = round_up(chunk, P.n >= 1024 * R ? 32 : 4);
         plan.chunk[p] = chunk;

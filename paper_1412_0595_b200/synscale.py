@@ -65,6 +65,7 @@ class ModelKind(enum.IntEnum):
     Izhikevich = L.MODEL_IZHIKEVICH
     PoissonSource = L.MODEL_POISSON
     CondLif = L.MODEL_CONDLIF
+    TraubMiles = L.MODEL_TRAUBMILES  # extension (F1): Traub-Miles HH
 
 
 class SynapseSign(enum.IntEnum):
@@ -181,6 +182,23 @@ class NetworkSpec:
 
 
 @dataclass
+class TraubMilesParams:
+    """Extension: GeNN's Traub-Miles HH neuron with CondLif-style
+    conductance synapses; not in the reference (parity is against oracle.c)."""
+    gNa: float = 7.15
+    ENa: float = 50.0
+    gK: float = 1.43
+    EK: float = -95.0
+    gl: float = 0.02672
+    El: float = -63.563
+    C: float = 0.143
+    eExcMV: float = 0.0
+    eInhMV: float = -92.0
+    tauSynMs: float = 3.0
+    substeps: int = 25
+
+
+@dataclass
 class MBodyBuildOptions:
     dtMs: float = 1.0
     durationMs: float = 1000.0
@@ -191,6 +209,8 @@ class MBodyBuildOptions:
     pnLhiWeight: float = 0.02
     lhiKcWeight: float = 0.01
     kcDnWeight: float = 0.01
+    kcModel: "ModelKind" = None  # extension: ModelKind.TraubMiles for HH KCs
+    kcHH: TraubMilesParams = field(default_factory=TraubMilesParams)
 
 
 @dataclass
@@ -224,6 +244,11 @@ class NetDesc:
                 d.tau_m_ms, d.e_leak_mv, d.v_thresh_mv = prm.tauMMs, prm.eLeakMV, prm.vThreshMV
                 d.v_reset_mv, d.e_exc_mv, d.e_inh_mv = prm.vResetMV, prm.eExcMV, prm.eInhMV
                 d.tau_syn_ms = prm.tauSynMs
+            elif isinstance(prm, TraubMilesParams):
+                d.hh_gna, d.hh_ena, d.hh_gk, d.hh_ek = prm.gNa, prm.ENa, prm.gK, prm.EK
+                d.hh_gl, d.hh_el, d.hh_c = prm.gl, prm.El, prm.C
+                d.e_exc_mv, d.e_inh_mv, d.tau_syn_ms = prm.eExcMV, prm.eInhMV, prm.tauSynMs
+                d.hh_substeps = int(prm.substeps)
             elif isinstance(prm, IzhikevichParams):
                 for attr, key in (("izh_a", "a"), ("izh_b", "b"), ("izh_c", "c"), ("izh_d", "d"),
                                   ("izh_noise", "noiseAmplitude"), ("izh_bias", "biasCurrent")):
@@ -263,6 +288,9 @@ def _spec_from_desc(d: L.ssb_net_desc) -> NetworkSpec:
         elif model == ModelKind.CondLif:
             prm = CondLifParams(p.tau_m_ms, p.e_leak_mv, p.v_thresh_mv, p.v_reset_mv,
                                 p.e_exc_mv, p.e_inh_mv, p.tau_syn_ms)
+        elif model == ModelKind.TraubMiles:
+            prm = TraubMilesParams(p.hh_gna, p.hh_ena, p.hh_gk, p.hh_ek, p.hh_gl, p.hh_el, p.hh_c,
+                                   p.e_exc_mv, p.e_inh_mv, p.tau_syn_ms, p.hh_substeps)
         else:
             n = p.size
             prm = IzhikevichParams(*[np.ctypeslib.as_array(getattr(p, f), (n,)).copy()
@@ -298,6 +326,13 @@ def build_mbody_net(nPN: int, nLHI: int, nKC: int, nDN: int, gScales: Dict[str, 
     o.tau_syn_ms = opt.lif.tauSynMs
     o.pn_kc_weight_hi, o.pn_lhi_weight = opt.pnKcWeightHi, opt.pnLhiWeight
     o.lhi_kc_weight, o.kc_dn_weight = opt.lhiKcWeight, opt.kcDnWeight
+    o.kc_model = int(opt.kcModel) if opt.kcModel is not None else L.MODEL_CONDLIF
+    h = opt.kcHH
+    o.hh_gna, o.hh_ena, o.hh_gk, o.hh_ek = h.gNa, h.ENa, h.gK, h.EK
+    o.hh_gl, o.hh_el, o.hh_c, o.hh_e_inh_mv, o.kc_tau_syn_ms = h.gl, h.El, h.C, h.eInhMV, h.tauSynMs
+    o.hh_substeps = h.substeps
+    if o.kc_model == L.MODEL_TRAUBMILES and h.eExcMV != opt.lif.eExcMV:
+        raise SpecError("the HH KCs share eExcMV with the CondLif populations in this builder")
     gs = (C.c_double * 4)(gScales["pn_kc"], gScales["pn_lhi"], gScales["lhi_kc"], gScales["kc_dn"])
     out = C.POINTER(L.ssb_net_desc)()
     err = _err()
@@ -432,6 +467,7 @@ class RunResult:
 
 _FIELDS = {"v": L.FIELD_V, "u": L.FIELD_U, "gExc": L.FIELD_GEXC, "gInh": L.FIELD_GINH,
            "excIn": L.FIELD_EXCIN, "inhIn": L.FIELD_INHIN}
+_HH_FIELDS = {"m": L.FIELD_M, "h": L.FIELD_H, "n": L.FIELD_N}  # Traub-Miles (extension)
 
 
 class Simulation:
@@ -504,7 +540,10 @@ class Simulation:
             self._check(lib.ssb_pull_state(self._h, pi, L.FIELD_FLAGGED, out.ctypes.data, 1))
             return out
         out = np.empty(n, np.float32)
-        self._check(lib.ssb_pull_state(self._h, pi, _FIELDS[fieldname], out.ctypes.data, n))
+        fid = _FIELDS.get(fieldname, _HH_FIELDS.get(fieldname))
+        if fid is None:
+            raise SpecError(f"unknown state field '{fieldname}'")
+        self._check(lib.ssb_pull_state(self._h, pi, fid, out.ctypes.data, n))
         return out
 
     def push(self, pop: Union[int, str], fieldname: str, values) -> None:
@@ -518,7 +557,9 @@ class Simulation:
             fid, n = L.FIELD_FLAGGED, 1
         else:
             a = np.ascontiguousarray(values, np.float32)
-            fid = _FIELDS[fieldname]
+            fid = _FIELDS.get(fieldname, _HH_FIELDS.get(fieldname))
+            if fid is None:
+                raise SpecError(f"unknown state field '{fieldname}'")
         if a.size != n:
             raise SpecError(f"state field '{fieldname}' holds {n} values, {a.size} given")
         self._check(lib.ssb_push_state(self._h, pi, fid, a.ctypes.data, n))

@@ -163,3 +163,11 @@ def izh_ff_spec(duration_ms: float = 200.0) -> S.NetworkSpec:
                            S.WeightDist.uniform(0.0, 0.05), 1.0, S.StorageKind.Dense),
     ]
     return spec
+
+
+def hh_mbody_spec(n_kc: int = 300, duration_ms: float = 30.0, seed: int = 7) -> S.NetworkSpec:
+    """Mushroom body with Traub-Miles HH KCs (extension)."""
+    o = S.MBodyBuildOptions(dtMs=0.1, durationMs=duration_ms, pnKcOutFraction=0.5,
+                            kcModel=S.ModelKind.TraubMiles)
+    return S.build_mbody_net(100, 20, n_kc, 100, {"pn_kc": 2.0, "pn_lhi": 1.0, "lhi_kc": 0.1,
+                                                  "kc_dn": 30.0 / n_kc}, seed, o)

@@ -496,3 +496,23 @@ def test_nccl_split_path_one_rank_matches_golden(golden, name):
             if p.model == S.ModelKind.PoissonSource and f in ("v", "gExc", "gInh"):
                 continue
             assert specs.sha(sim.pull(pi, f)) == h, (p.name, f)
+
+
+@pytest.mark.parametrize("kw", [{"window": 1}, {"window": 64}, {"window": 64, "virtualWorld": 2,
+                                                                 "shardMinSize": 32}])
+def test_traubmiles_kcs_match_restatement(oracle_mod, kw):
+    """Traub-Miles HH KCs (extension F1, no reference implementation): the
+    device equals the CPU restatement in oracle.c bit for bit (same custom
+    exp, same operation order) -- state every 100 steps and the raster."""
+    spec = specs.hh_mbody_spec()
+    g = gpu_sim(spec, **kw)
+    o = cpu_sim(oracle_mod, spec)
+    kc = spec.pop_index("kc")
+    for t in range(3):
+        g.step(100)
+        o.step(100)
+        for f in ("v", "gExc", "gInh", "m", "h", "n", "excIn", "inhIn"):
+            assert specs.bits_equal(g.pull(kc, f), o.state(kc, f)), (t, f)
+    rg, ro = g.finish(), o.finish()
+    assert np.array_equal(rg.raster.neuron, ro[2]) and np.array_equal(rg.raster.step, ro[0])
+    assert np.count_nonzero(rg.raster.population == kc) > 100
