@@ -412,12 +412,17 @@ struct DeviceEngine::Impl {
     bool is_wide(long long blocks, int smem) const {
         return blocks >= smCount / 4 && smem >= 32 * 1024;
     }
+    cudaStream_t lastWideStream = nullptr;
     void before_wide(cudaStream_t s) {
-        if (multiStream && lastWide) CK(cudaStreamWaitEvent(s, lastWide, 0));
+        // same stream: ordered anyway (an event edge would also turn the
+        // programmatic launch of the next update into a full dependency)
+        if (multiStream && lastWide && lastWideStream != s)
+            CK(cudaStreamWaitEvent(s, lastWide, 0));
     }
     void after_wide(cudaStream_t s) {
         if (!multiStream) return;
         lastWide = capture_event();
+        lastWideStream = s;
         CK(cudaEventRecord(lastWide, s));
     }
     std::int64_t launchesDone = 0;
@@ -1030,27 +1035,22 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
         const ssbk::PopDev& K = P.kdev[b];
         const bool wide = is_wide(P.grid, P.smemBytes);
         if (wide) before_wide(sm);
+        auto update = [&](const char* tag, auto kernel) {
+            launch(tag + P.name, [&] {
+                kernel<<<P.grid, P.block, P.smemBytes, sm>>>(K, P.accb[b][0], P.accb[b][1],
+                                                             P.stage[0], P.stage[1], W, P.tileN,
+                                                             P.chunk, P.offIn, P.offBits);
+            });
+        };
         if (P.kind == kIzhikevich) {
             launch("gaussian_window:" + P.name, [&] {
                 ssbk::gaussian_window_kernel<<<1, 320, 0, sm>>>(K, W);
             });
-            launch("izh_window:" + P.name, [&] {
-                ssbk::izh_window_kernel<<<P.grid, P.block, P.smemBytes, sm>>>(
-                    K, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk,
-                    P.offIn, P.offBits);
-            });
+            update("izh_window:", ssbk::izh_window_kernel);
         } else if (P.kind == kTraubMiles) {
-            launch("hh_window:" + P.name, [&] {
-                ssbk::hh_window_kernel<<<P.grid, P.block, P.smemBytes, sm>>>(
-                    K, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk,
-                    P.offIn, P.offBits);
-            });
+            update("hh_window:", ssbk::hh_window_kernel);
         } else {
-            launch("condlif_window:" + P.name, [&] {
-                ssbk::condlif_window_kernel<<<P.grid, P.block, P.smemBytes, sm>>>(
-                    K, P.accb[b][0], P.accb[b][1], P.stage[0], P.stage[1], W, P.tileN, P.chunk,
-                    P.offIn, P.offBits);
-            });
+            update("condlif_window:", ssbk::condlif_window_kernel);
         }
         // the next wide kernel may start right after the update: compaction
         // (on sp) feeds only this window's consumers
@@ -1146,6 +1146,7 @@ void DeviceEngine::Impl::enqueue_windows(int W, int M) {
     evUsed = 0;
     multiStream = multi;
     lastWide = nullptr;
+    lastWideStream = nullptr;
     lastCollective = nullptr;
     auto mark = [&](int sidx) -> cudaEvent_t {
         if (!multi) return nullptr;

@@ -13,12 +13,12 @@ import specs  # noqa: E402
 from paper_1412_0595_b200 import synscale as S  # noqa: E402
 
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 256
-spec, mode = specs.config_spec(3, 400.0)
+spec, mode = specs.config_spec(3, (4 + int(os.environ.get("TL_WINDOWS", "8")) + 1) * W * 0.1)
 sim = S.Simulation(spec, mode, S.EngineOptions(window=W))
 sim.step(W * 4)
 sim.sync()
 open(path, "w").close()
-sim.step(W * 8)
+sim.step(W * int(os.environ.get("TL_WINDOWS", "8")))
 sim.sync()
 sim.kernel_stats()  # harvest
 rows = [l.split() for l in open(path)]
@@ -26,7 +26,8 @@ rows = [(n, float(a), float(b)) for n, a, b in rows]
 t0 = min(r[1] for r in rows)
 rows = [(n, a - t0, b - t0) for n, a, b in rows]
 span = max(r[2] for r in rows)
-print(f"{len(rows)} launches, {span:.1f} us for 8 windows -> {span / 8:.1f} us/window, "
-      f"{span / 8 / W * 1e3:.1f} ns/step")
+nw = int(os.environ.get("TL_WINDOWS", "8"))
+print(f"{len(rows)} launches, {span:.1f} us for {nw} windows -> {span / nw:.1f} us/window, "
+      f"{span / nw / W * 1e3:.1f} ns/step")
 for n, a, b in sorted(rows, key=lambda r: r[1])[:int(os.environ.get("TL_ROWS", "40"))]:
     print(f"{n:28s} {a:9.1f} {b:9.1f} {b - a:8.1f}")
