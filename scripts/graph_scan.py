@@ -13,8 +13,10 @@ if len(sys.argv) > 1:  # child: one M
     M = int(sys.argv[1])
     n = 256 * 64
     spec, mode = specs.config_spec(3, (n * 2 + 512) * 0.1)
-    sim = S.Simulation(spec, mode, S.EngineOptions(window=256,
-                                                   blockSize=int(os.environ.get("GS_BS", "0"))))
+    split = os.environ.get("GS_SPLIT") == "1"  # the exchange path on a one-rank communicator
+    sim = S.Simulation(spec, mode, S.EngineOptions(
+        window=256, blockSize=int(os.environ.get("GS_BS", "0")),
+        **({"world": 1, "rank": 0, "commId": S.comm_unique_id()} if split else {})))
     sim.step(n)
     sim.sync()
     st = torch.cuda.ExternalStream(sim.stream())
