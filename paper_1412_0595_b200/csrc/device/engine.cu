@@ -1099,6 +1099,14 @@ void DeviceEngine::Impl::assemble_compact(int pi, int W, int b, cudaStream_t s) 
     launchStream = s;
     auto& P = pops[pi];
     const ssbk::PopDev& D = P.devb[b];
+    if (P.nwGlobal <= 32) {  // small population: one block, a warp per step
+        launch("assemble_compact:" + P.name, [&] {
+            ssbk::assemble_compact_small_kernel<<<1, 256, 0, s>>>(
+                P.gathered[b], W, P.nwords, P.shardChunk, P.nGlobal, P.nwGlobal, D.bits, D.list,
+                D.count);
+        });
+        return;
+    }
     const int bs = std::min(1024, round_up(P.nwGlobal, 32));
     launch("assemble_bits:" + P.name, [&] {
         ssbk::assemble_bits_kernel<<<W, bs, 0, s>>>(P.gathered[b], W, P.nwords, P.shardChunk,

@@ -14,7 +14,9 @@ from paper_1412_0595_b200 import synscale as S  # noqa: E402
 
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 spec, mode = specs.config_spec(3, (4 + int(os.environ.get("TL_WINDOWS", "8")) + 1) * W * 0.1)
-sim = S.Simulation(spec, mode, S.EngineOptions(window=W))
+split = os.environ.get("TL_SPLIT") == "1"  # exchange path on a one-rank communicator
+sim = S.Simulation(spec, mode, S.EngineOptions(
+    window=W, **({"world": 1, "rank": 0, "commId": S.comm_unique_id()} if split else {})))
 sim.step(W * 4)
 sim.sync()
 open(path, "w").close()
