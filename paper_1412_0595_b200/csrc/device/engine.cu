@@ -449,16 +449,7 @@ struct DeviceEngine::Impl {
     bool usePipe = false;
     void launch_dense(const ssbk::GroupDev& G, const std::string& gname, const char* tag,
                       float* out, long long stride, int wLo, int nW, int first, cudaStream_t s) {
-        if (G.nPost % 4 == 0 && G.nPost <= 32 && G.nPost > 0 && !usePipe) {
-            int c16p = 1;  // lanes per step: a power of two >= nPost / 4
-            while (c16p < G.nPost / 4) c16p *= 2;
-            const int stepsPerWarp = 32 / c16p;
-            const int warps = (nW + stepsPerWarp - 1) / stepsPerWarp;
-            launch(std::string(tag) + gname, [&] {
-                ssbk::dense_window_narrow_kernel<<<(warps + 3) / 4, 128, 0, s>>>(
-                    G, out, stride, wLo, nW, first, c16p);
-            });
-        } else if (G.nPost % 4 == 0 && !usePipe) {
+        if (G.nPost % 4 == 0 && !usePipe) {
             dim3 grid((G.nPost + ssbk::kWarpSlab - 1) / ssbk::kWarpSlab, nW);
             launch(std::string(tag) + gname, [&] {
                 ssbk::dense_window_warp_kernel<<<grid, 32, kWarpRingBytes, s>>>(G, out, stride,
@@ -1099,9 +1090,9 @@ void DeviceEngine::Impl::assemble_compact(int pi, int W, int b, cudaStream_t s) 
     launchStream = s;
     auto& P = pops[pi];
     const ssbk::PopDev& D = P.devb[b];
-    if (P.nwGlobal <= 32) {  // small population: one block, a warp per step
+    if (P.nwGlobal <= 32) {  // small population: a block per step, a thread per neuron
         launch("assemble_compact:" + P.name, [&] {
-            ssbk::assemble_compact_small_kernel<<<1, 256, 0, s>>>(
+            ssbk::assemble_compact_small_kernel<<<W, 32 * P.nwGlobal, 0, s>>>(
                 P.gathered[b], W, P.nwords, P.shardChunk, P.nGlobal, P.nwGlobal, D.bits, D.list,
                 D.count);
         });
