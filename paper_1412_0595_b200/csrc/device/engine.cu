@@ -223,6 +223,7 @@ struct DeviceEngine::Impl {
     EngineConfig cfg;
     int world = 1;              // ranks (or virtual shards) the network is split over
     bool virtualShard = false;  // one of several shards in this process (exchange by copies)
+    bool emulateExchange = false;  // SSB_EMULATE_EXCHANGE diagnostic (see the constructor)
     bool serial = false;        // one stream, no graphs (profiling, virtual shards)
     bool ownsStream = true;
     std::unique_ptr<Comm> comm;  // NCCL, one process per GPU
@@ -449,7 +450,14 @@ struct DeviceEngine::Impl {
     bool usePipe = false;
     void launch_dense(const ssbk::GroupDev& G, const std::string& gname, const char* tag,
                       float* out, long long stride, int wLo, int nW, int first, cudaStream_t s) {
-        if (G.nPost % 4 == 0 && !usePipe) {
+        if (G.nPost % 4 == 0 && G.nPost <= ssbk::kChainMaxPost && !usePipe) {
+            const int smem = ssbk::kChainStages * ssbk::kChainPer *
+                             (ssbk::kChainCopiers / (G.nPost / 4)) * G.nPost * 4;
+            launch(std::string(tag) + gname, [&] {
+                ssbk::dense_window_chain_kernel<<<dim3(1, nW), 128, smem, s>>>(G, out, stride, wLo,
+                                                                              first);
+            });
+        } else if (G.nPost % 4 == 0 && !usePipe) {
             dim3 grid((G.nPost + ssbk::kWarpSlab - 1) / ssbk::kWarpSlab, nW);
             launch(std::string(tag) + gname, [&] {
                 ssbk::dense_window_warp_kernel<<<grid, 32, kWarpRingBytes, s>>>(G, out, stride,
@@ -967,7 +975,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         }
     }
     // capture streams: one per population, one for deliver + raster
-    auxStreams.resize(3 * nPops + 1);
+    // 3 per population, the raster's, then a second group stream per population
+    auxStreams.resize(4 * nPops + 1);
     for (auto& s : auxStreams) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
 
     // kernels with large dynamic shared tiles (the limit is per function and
@@ -985,6 +994,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     allow(reinterpret_cast<const void*>(&ssbk::hh_window_kernel), std::max(maxSmem, 4096));
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_warp_kernel), kWarpRingBytes);
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_pipe_kernel), ring_smem());
+    allow(reinterpret_cast<const void*>(&ssbk::dense_window_chain_kernel), ssbk::kChainSmem);
     if (const char* e = std::getenv("SSB_DENSE_KERNEL")) usePipe = std::string(e) == "pipe";
     if (const char* e = std::getenv("SSB_TIMELINE")) timelinePath = e;
     CK(cudaStreamSynchronize(stream));
@@ -1079,6 +1089,11 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
                 lastCollective = capture_event();
                 CK(cudaEventRecord(lastCollective, sp));
             }
+        } else if (emulateExchange) {
+            const std::size_t bytes = static_cast<std::size_t>(W) * P.nwords * 4;
+            for (int r = 0; r < world; ++r)
+                CK(cudaMemcpyAsync(reinterpret_cast<char*>(P.gathered[b]) + r * bytes,
+                                   P.kdev[b].bits, bytes, cudaMemcpyDeviceToDevice, sp));
         }
         if (!virtualShard) assemble_compact(pi, W, b, sp);  // virtual: after the shard copies
     }
@@ -1179,8 +1194,14 @@ void DeviceEngine::Impl::enqueue_windows(int W, int M) {
             // extra streams only where they carry work (a graph's branches share
             // a few hardware queues: unused parallelism costs false dependencies)
             const int sm = 3 * pi + 1;
-            const int sg = P.acc[0].mode == ssbk::kAccBuffered || P.acc[1].mode == ssbk::kAccBuffered
-                               ? 3 * pi : sm;
+            const bool buffered =
+                P.acc[0].mode == ssbk::kAccBuffered || P.acc[1].mode == ssbk::kAccBuffered;
+            // narrow gathers (a rank's few DN columns) are latency-bound chains
+            // with a block per step: consecutive windows' gathers write
+            // different buffer sets, so they alternate between two streams
+            // and overlap
+            const bool narrow = buffered && P.n > 0 && P.n <= ssbk::kChainMaxPost;
+            const int sg = !buffered ? sm : (narrow && (m & 1)) ? rs + 1 + pi : 3 * pi;
             const int sp = (P.grid > 1 && P.n > 0) || P.sharded ? 3 * pi + 2 : sm;
             for (int x : {sg, sm}) {
                 for (int q : P.prePops) after(x, kdone[q][m]);
@@ -1318,7 +1339,13 @@ DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfgIn)
     CK(cudaSetDevice(cfg.device));
     const bool virt = cfg.virtualWorld > 1;
     const int R = virt ? cfg.virtualWorld : std::max(1, cfg.world);
-    if (!virt && R > 1 && !cfg.hasCommId)
+    // diagnostic (SSB_EMULATE_EXCHANGE=1): one rank of a world of R on its own,
+    // the all-gather replaced by R copies of the local bits -- the rank's
+    // real per-window work (global spike lists R x as long) with meaningless
+    // dynamics, for timing weak scaling on one GPU
+    const bool emulate = !virt && R > 1 && !cfg.hasCommId && std::getenv("SSB_EMULATE_EXCHANGE") &&
+                         std::string(std::getenv("SSB_EMULATE_EXCHANGE")) == "1";
+    if (!virt && R > 1 && !cfg.hasCommId && !emulate)
         throw synscale::SpecError("a multi-GPU run needs a communicator id (ssb_comm_unique_id)");
     if (!virt && R > 1 && (cfg.rank < 0 || cfg.rank >= R))
         throw synscale::SpecError("rank " + std::to_string(cfg.rank) + " outside a world of " +
@@ -1334,6 +1361,7 @@ DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfgIn)
         m.world = R;
         m.smCount = smCount;
         m.virtualShard = virt;
+        m.emulateExchange = emulate;
         if (virt) {  // lockstep across shards on one stream
             m.serial = true;
             m.cfg.useGraphs = false;
@@ -1347,7 +1375,7 @@ DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfgIn)
         try {
             ShardStore store;
             const HostNet local = split ? shard_net(net, plan, rank, store) : HostNet{};
-            if (split && !virt) m.comm = std::make_unique<Comm>(R, rank, cfg.commId.data());
+            if (split && !virt && !emulate) m.comm = std::make_unique<Comm>(R, rank, cfg.commId.data());
             m.build(split ? local : net);
         } catch (...) {
             m.release();

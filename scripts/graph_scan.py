@@ -1,5 +1,11 @@
 """µs per window vs windows per graph launch (config 3, W = 256), steps a multiple of
-256 x M so every launch is a full M-window graph."""
+256 x M so every launch is a full M-window graph.
+
+GS_SPLIT=1: the exchange path on a one-rank communicator.
+GS_EMULATE=R: one rank of bench.py's weak split world of R (R x 100k KC, this
+rank's 100k) with the all-gather emulated by copies (SSB_EMULATE_EXCHANGE:
+the rank's real work, meaningless dynamics) -- weak scaling on one GPU.
+"""
 import os
 import subprocess
 import sys
@@ -12,11 +18,17 @@ if len(sys.argv) > 1:  # child: one M
     from paper_1412_0595_b200 import synscale as S
     M = int(sys.argv[1])
     n = 256 * 64
-    spec, mode = specs.config_spec(3, (n * 2 + 512) * 0.1)
-    split = os.environ.get("GS_SPLIT") == "1"  # the exchange path on a one-rank communicator
+    emu = int(os.environ.get("GS_EMULATE", "0"))
+    if emu > 1:
+        os.environ["SSB_EMULATE_EXCHANGE"] = "1"
+        spec, mode = specs.mbody_spec(100_000 * emu, 0.05, (n * 2 + 512) * 0.1), S.StorageMode.FromSpec
+        extra = {"world": emu, "rank": emu // 2}
+    else:
+        spec, mode = specs.config_spec(3, (n * 2 + 512) * 0.1)
+        split = os.environ.get("GS_SPLIT") == "1"
+        extra = {"world": 1, "rank": 0, "commId": S.comm_unique_id()} if split else {}
     sim = S.Simulation(spec, mode, S.EngineOptions(
-        window=256, blockSize=int(os.environ.get("GS_BS", "0")),
-        **({"world": 1, "rank": 0, "commId": S.comm_unique_id()} if split else {})))
+        window=256, blockSize=int(os.environ.get("GS_BS", "0")), **extra))
     sim.step(n)
     sim.sync()
     st = torch.cuda.ExternalStream(sim.stream())

@@ -13,10 +13,17 @@ import specs  # noqa: E402
 from paper_1412_0595_b200 import synscale as S  # noqa: E402
 
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 256
-spec, mode = specs.config_spec(3, (4 + int(os.environ.get("TL_WINDOWS", "8")) + 1) * W * 0.1)
-split = os.environ.get("TL_SPLIT") == "1"  # exchange path on a one-rank communicator
-sim = S.Simulation(spec, mode, S.EngineOptions(
-    window=W, **({"world": 1, "rank": 0, "commId": S.comm_unique_id()} if split else {})))
+dur = (4 + int(os.environ.get("TL_WINDOWS", "8")) + 1) * W * 0.1
+emu = int(os.environ.get("TL_EMULATE", "0"))  # one rank of a weak world (graph_scan.py)
+if emu > 1:
+    os.environ["SSB_EMULATE_EXCHANGE"] = "1"
+    spec, mode = specs.mbody_spec(100_000 * emu, 0.05, dur), S.StorageMode.FromSpec
+    extra = {"world": emu, "rank": emu // 2}
+else:
+    spec, mode = specs.config_spec(3, dur)
+    split = os.environ.get("TL_SPLIT") == "1"  # exchange path on a one-rank communicator
+    extra = {"world": 1, "rank": 0, "commId": S.comm_unique_id()} if split else {}
+sim = S.Simulation(spec, mode, S.EngineOptions(window=W, **extra))
 sim.step(W * 4)
 sim.sync()
 open(path, "w").close()
