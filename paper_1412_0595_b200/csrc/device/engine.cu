@@ -181,6 +181,16 @@ bool kernel_attributes(const std::string& name, int& regs, int& sharedBytes, int
 
 // ---------------------------------------------------------------------------
 
+using ChainFn = void (*)(ssbk::GroupDev, float*, long long, int, int);
+ChainFn chain_kernel(int nPost) {  // nPost % 4 == 0, <= kChainMaxPost
+    static constexpr ChainFn k[8] = {
+        ssbk::dense_window_chain_kernel<4>,  ssbk::dense_window_chain_kernel<8>,
+        ssbk::dense_window_chain_kernel<12>, ssbk::dense_window_chain_kernel<16>,
+        ssbk::dense_window_chain_kernel<20>, ssbk::dense_window_chain_kernel<24>,
+        ssbk::dense_window_chain_kernel<28>, ssbk::dense_window_chain_kernel<32>};
+    return k[nPost / 4 - 1];
+}
+
 struct DeviceEngine::Impl {
     // window-buffer sets: every window of a graph launch gets its own set of
     // spike lists / bitmasks / buffered inputs, so no window waits for an
@@ -454,8 +464,7 @@ struct DeviceEngine::Impl {
             const int smem = ssbk::kChainStages * ssbk::kChainPer *
                              (ssbk::kChainCopiers / (G.nPost / 4)) * G.nPost * 4;
             launch(std::string(tag) + gname, [&] {
-                ssbk::dense_window_chain_kernel<<<dim3(1, nW), 128, smem, s>>>(G, out, stride, wLo,
-                                                                              first);
+                chain_kernel(G.nPost)<<<dim3(1, nW), ssbk::kChainCopiers + 32, smem, s>>>(G, out, stride, wLo, first);
             });
         } else if (G.nPost % 4 == 0 && !usePipe) {
             dim3 grid((G.nPost + ssbk::kWarpSlab - 1) / ssbk::kWarpSlab, nW);
@@ -994,7 +1003,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     allow(reinterpret_cast<const void*>(&ssbk::hh_window_kernel), std::max(maxSmem, 4096));
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_warp_kernel), kWarpRingBytes);
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_pipe_kernel), ring_smem());
-    allow(reinterpret_cast<const void*>(&ssbk::dense_window_chain_kernel), ssbk::kChainSmem);
+    for (int np = 4; np <= ssbk::kChainMaxPost; np += 4)
+        allow(reinterpret_cast<const void*>(chain_kernel(np)), ssbk::kChainSmem);
     if (const char* e = std::getenv("SSB_DENSE_KERNEL")) usePipe = std::string(e) == "pipe";
     if (const char* e = std::getenv("SSB_TIMELINE")) timelinePath = e;
     CK(cudaStreamSynchronize(stream));
@@ -1068,7 +1078,7 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
         edge(sm, sp);
         launchStream = sp;
         if (P.grid > 1 && !P.sharded) {
-            const int bs = std::min(1024, round_up(P.nwords, 32));
+            const int bs = std::min(1024, round_up((P.nwords + ssbk::kCompactK - 1) / ssbk::kCompactK, 32));
             launch("compact_window:" + P.name, [&] {
                 ssbk::compact_window_kernel<<<W, bs, 0, sp>>>(K.bits, P.nwords, P.n, K.list, K.count);
             });
@@ -1113,13 +1123,11 @@ void DeviceEngine::Impl::assemble_compact(int pi, int W, int b, cudaStream_t s) 
         });
         return;
     }
-    const int bs = std::min(1024, round_up(P.nwGlobal, 32));
-    launch("assemble_bits:" + P.name, [&] {
-        ssbk::assemble_bits_kernel<<<W, bs, 0, s>>>(P.gathered[b], W, P.nwords, P.shardChunk,
-                                                    P.nGlobal, P.nwGlobal, D.bits);
-    });
-    launch("compact_window:" + P.name, [&] {
-        ssbk::compact_window_kernel<<<W, bs, 0, s>>>(D.bits, P.nwGlobal, P.nGlobal, D.list, D.count);
+    const int bs = std::min(1024, round_up((P.nwGlobal + ssbk::kCompactK - 1) / ssbk::kCompactK, 32));
+    launch("assemble_compact:" + P.name, [&] {
+        ssbk::assemble_compact_kernel<<<W, bs, 0, s>>>(P.gathered[b], W, P.nwords, P.shardChunk,
+                                                       P.nGlobal, P.nwGlobal, D.bits, D.list,
+                                                       D.count);
     });
 }
 
@@ -1149,7 +1157,7 @@ void DeviceEngine::Impl::enqueue_tail(int W, int b, cudaStream_t s) {
         }
     }
     launch("raster_window", [&] {
-        ssbk::raster_window_kernel<<<W * raster.nPops, 128, 0, s>>>(rasterb[b], W);
+        ssbk::raster_window_kernel<<<W * raster.nPops, 256, 0, s>>>(rasterb[b], W);
     });
 }
 
