@@ -8,7 +8,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <array>
 #include <map>
+#include <utility>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -182,14 +184,16 @@ bool kernel_attributes(const std::string& name, int& regs, int& sharedBytes, int
 // ---------------------------------------------------------------------------
 
 using ChainFn = void (*)(ssbk::GroupDev, float*, long long, int, int);
+template <int... NP>
+constexpr std::array<ChainFn, sizeof...(NP)> chain_table(std::integer_sequence<int, NP...>) {
+    return {ssbk::dense_window_chain_kernel<4 * (NP + 1)>...};
+}
 ChainFn chain_kernel(int nPost) {  // nPost % 4 == 0, <= kChainMaxPost
-    static constexpr ChainFn k[8] = {
-        ssbk::dense_window_chain_kernel<4>,  ssbk::dense_window_chain_kernel<8>,
-        ssbk::dense_window_chain_kernel<12>, ssbk::dense_window_chain_kernel<16>,
-        ssbk::dense_window_chain_kernel<20>, ssbk::dense_window_chain_kernel<24>,
-        ssbk::dense_window_chain_kernel<28>, ssbk::dense_window_chain_kernel<32>};
+    static constexpr auto k =
+        chain_table(std::make_integer_sequence<int, ssbk::kChainMaxPost / 4>{});
     return k[nPost / 4 - 1];
 }
+int chain_threads(int nPost) { return ssbk::kChainCopiers + 32 * ((nPost + 31) / 32); }
 
 struct DeviceEngine::Impl {
     // window-buffer sets: every window of a graph launch gets its own set of
@@ -335,6 +339,10 @@ struct DeviceEngine::Impl {
     // harvest() appends "name start_us end_us" lines (relative to the first
     // launch) to the file.
     std::string timelinePath;
+    int prioHigh = 0;          // the device's greatest launch priority
+    bool usePriority = true;   // SSB_PRIORITY=0 disables the update priority
+    std::string tracePath;  // SSB_TRACE: per-block records written at release
+    unsigned long long* traceBuf = nullptr;
     cudaEvent_t timelineBase = nullptr;
     cudaStream_t launchStream = nullptr;  // stream of the launches being enqueued
     bool timed() const { return cfg.profile || !timelinePath.empty(); }
@@ -464,7 +472,8 @@ struct DeviceEngine::Impl {
             const int smem = ssbk::kChainStages * ssbk::kChainPer *
                              (ssbk::kChainCopiers / (G.nPost / 4)) * G.nPost * 4;
             launch(std::string(tag) + gname, [&] {
-                chain_kernel(G.nPost)<<<dim3(1, nW), ssbk::kChainCopiers + 32, smem, s>>>(G, out, stride, wLo, first);
+                chain_kernel(G.nPost)<<<dim3(1, nW), chain_threads(G.nPost), smem, s>>>(G, out, stride,
+                                                                                   wLo, first);
             });
         } else if (G.nPost % 4 == 0 && !usePipe) {
             dim3 grid((G.nPost + ssbk::kWarpSlab - 1) / ssbk::kWarpSlab, nW);
@@ -986,6 +995,9 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     // capture streams: one per population, one for deliver + raster
     // 3 per population, the raster's, then a second group stream per population
     auxStreams.resize(4 * nPops + 1);
+    int leastPrio = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&leastPrio, &prioHigh));
+    usePriority = !std::getenv("SSB_PRIORITY") || std::string(std::getenv("SSB_PRIORITY")) != "0";
     for (auto& s : auxStreams) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
 
     // kernels with large dynamic shared tiles (the limit is per function and
@@ -1007,6 +1019,16 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         allow(reinterpret_cast<const void*>(chain_kernel(np)), ssbk::kChainSmem);
     if (const char* e = std::getenv("SSB_DENSE_KERNEL")) usePipe = std::string(e) == "pipe";
     if (const char* e = std::getenv("SSB_TIMELINE")) timelinePath = e;
+    if (const char* e = std::getenv("SSB_TRACE")) {  // per-block trace (scripts/trace_kc.py)
+        tracePath = e;
+        const unsigned cap = 1u << 22;
+        traceBuf = alloc<unsigned long long>(4ull * cap);
+        unsigned long long* p = traceBuf;
+        const unsigned zero = 0;
+        CK(cudaMemcpyToSymbol(ssbk::g_trace, &p, sizeof(p)));
+        CK(cudaMemcpyToSymbol(ssbk::g_traceN, &zero, sizeof(zero)));
+        CK(cudaMemcpyToSymbol(ssbk::g_traceCap, &cap, sizeof(cap)));
+    }
     CK(cudaStreamSynchronize(stream));
 }
 
@@ -1057,9 +1079,23 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
         if (wide) before_wide(sm);
         auto update = [&](const char* tag, auto kernel) {
             launch(tag + P.name, [&] {
-                kernel<<<P.grid, P.block, P.smemBytes, sm>>>(K, P.accb[b][0], P.accb[b][1],
-                                                             P.stage[0], P.stage[1], W, P.tileN,
-                                                             P.chunk, P.offIn, P.offBits);
+                // multi-block updates launch at the highest priority (a launch
+                // attribute, kept by the graph's kernel node): when a window's
+                // update ends, the next one's blocks take the freed SMs ahead of
+                // the gather blocks queued behind them -- otherwise its last
+                // blocks start 15-45 us late (device trace, scripts/trace_kc.py)
+                cudaLaunchConfig_t lc{};
+                lc.gridDim = dim3(P.grid);
+                lc.blockDim = dim3(P.block);
+                lc.dynamicSmemBytes = P.smemBytes;
+                lc.stream = sm;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributePriority;
+                at[0].val.priority = prioHigh;
+                lc.attrs = at;
+                lc.numAttrs = P.grid > 1 && usePriority ? 1 : 0;
+                CK(cudaLaunchKernelEx(&lc, kernel, K, P.accb[b][0], P.accb[b][1], P.stage[0],
+                                      P.stage[1], W, P.tileN, P.chunk, P.offIn, P.offBits));
             });
         };
         if (P.kind == kIzhikevich) {
@@ -1446,6 +1482,21 @@ void DeviceEngine::lockstep(int W) {
 
 void DeviceEngine::Impl::release() {
     join_copier();
+    if (traceBuf && !tracePath.empty()) {
+        cudaDeviceSynchronize();
+        unsigned n = 0;
+        cudaMemcpyFromSymbol(&n, ssbk::g_traceN, sizeof(n));
+        n = std::min(n, 1u << 22);
+        std::vector<unsigned long long> h(4ull * n);
+        cudaMemcpy(h.data(), traceBuf, h.size() * 8, cudaMemcpyDeviceToHost);
+        if (FILE* f = std::fopen(tracePath.c_str(), "wb")) {
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
+        unsigned long long* nul = nullptr;
+        cudaMemcpyToSymbol(ssbk::g_trace, &nul, sizeof(nul));
+        tracePath.clear();
+    }
     if (copyStream) cudaStreamDestroy(copyStream), copyStream = nullptr;
     for (auto& p : pinned)
         if (p) cudaFreeHost(p), p = nullptr;
