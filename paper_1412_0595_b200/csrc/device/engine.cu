@@ -199,7 +199,7 @@ struct DeviceEngine::Impl {
     // window-buffer sets: every window of a graph launch gets its own set of
     // spike lists / bitmasks / buffered inputs, so no window waits for an
     // earlier one's consumers to free a buffer (launches serialise anyway)
-    static constexpr int kMaxSets = 16;
+    static constexpr int kMaxSets = 48;
     int nSets = 2;
     struct PopRt {
         int kind = 0, n = 0, nwords = 0;
@@ -273,7 +273,7 @@ struct DeviceEngine::Impl {
     // near full.  The cursor after each window is copied asynchronously to a
     // pinned ring; the host never runs more than kRing windows ahead, so the
     // arena fill is known up to kRing windows of worst-case growth.
-    static constexpr int kRing = 4;
+    static constexpr int kRing = 2;
     ssbk::RasterDev raster{};
     std::int64_t rasterCap = 0;
     long long* ringVal = nullptr;  // pinned
@@ -757,8 +757,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         // (every neuron spiking every step); beyond 4G events (16 GB per arena,
         // two arenas) shrink the launch.
         const std::int64_t perWin = static_cast<std::int64_t>(Wmax) * totalNeurons;
-        while (graphWindows > 1 && (kRing + 1) * perWin * graphWindows > (std::int64_t(1) << 32))
-            graphWindows /= 2;
+        const std::int64_t fit = (std::int64_t(1) << 32) / ((kRing + 1) * std::max<std::int64_t>(perWin, 1));
+        graphWindows = static_cast<int>(std::clamp<std::int64_t>(fit, 1, graphWindows));
     }
     nSets = std::clamp(graphWindows, 2, kMaxSets);
 
