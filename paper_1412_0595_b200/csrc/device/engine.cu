@@ -340,6 +340,7 @@ struct DeviceEngine::Impl {
     // launch) to the file.
     std::string timelinePath;
     int prioHigh = 0;          // the device's greatest launch priority
+    bool usePdl = false;       // SSB_PDL=1: programmatic launch of consecutive updates
     bool usePriority = true;   // SSB_PRIORITY=0 disables the update priority
     std::string tracePath;  // SSB_TRACE: per-block records written at release
     unsigned long long* traceBuf = nullptr;
@@ -998,6 +999,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     int leastPrio = 0;
     CK(cudaDeviceGetStreamPriorityRange(&leastPrio, &prioHigh));
     usePriority = !std::getenv("SSB_PRIORITY") || std::string(std::getenv("SSB_PRIORITY")) != "0";
+    usePdl = std::getenv("SSB_PDL") && std::string(std::getenv("SSB_PDL")) == "1";
     for (auto& s : auxStreams) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
 
     // kernels with large dynamic shared tiles (the limit is per function and
@@ -1089,11 +1091,24 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
                 lc.blockDim = dim3(P.block);
                 lc.dynamicSmemBytes = P.smemBytes;
                 lc.stream = sm;
-                cudaLaunchAttribute at[1];
-                at[0].id = cudaLaunchAttributePriority;
-                at[0].val.priority = prioHigh;
+                cudaLaunchAttribute at[2];
+                int na = 0;
+                if (P.grid > 1 && usePriority) {
+                    at[na].id = cudaLaunchAttributePriority;
+                    at[na++].val.priority = prioHigh;
+                }
+                // programmatic dependent launch: the stream's previous kernel
+                // (the previous window's update) lets this grid launch in its
+                // last chunk, and this grid waits for it to complete with
+                // griddepcontrol.wait before anything else (kernels.cuh
+                // window_body) -- whatever the previous kernel is, so the
+                // stream order stays a full dependency
+                if (P.grid > 1 && usePdl) {
+                    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                    at[na++].val.programmaticStreamSerializationAllowed = 1;
+                }
                 lc.attrs = at;
-                lc.numAttrs = P.grid > 1 && usePriority ? 1 : 0;
+                lc.numAttrs = na;
                 CK(cudaLaunchKernelEx(&lc, kernel, K, P.accb[b][0], P.accb[b][1], P.stage[0],
                                       P.stage[1], W, P.tileN, P.chunk, P.offIn, P.offBits));
             });

@@ -37,7 +37,7 @@ base = t0.min()
 t0, t1 = (t0 - base) / 1e3, (t1 - base) / 1e3  # us
 nkc = 100_000 * max(1, emu) // max(1, emu) if emu <= 1 else None
 kc_tag = max(int(x) for x in set(tag.tolist()) if x < 0xfffffff0)
-names = {kc_tag: "kc", 20: "lhi", 100: "dn", 0xffffffff: "kc_dn"}
+names = {kc_tag: "kc", 20: "lhi", 100: "dn", 0xffffffff: "kc_dn", 0xfffffffd: "raster"}
 # the last nwin windows' KC launches: split KC blocks into launches by start gaps
 k = np.where(tag == kc_tag)[0]
 order = k[np.argsort(t0[k])]
@@ -63,3 +63,20 @@ for tg, nm in names.items():
     if m.any():
         d = t1[m] - t0[m]
         print(f"{nm:6s} blocks {m.sum():7d} block-duration median {np.median(d):7.1f} us  p90 {np.percentile(d, 90):7.1f}")
+
+# what occupied SMs while the last KC blocks waited: other blocks running at
+# the moment each late KC block started
+late = []
+for L in launches[2:]:
+    s0 = t0[L].min()
+    for i in L:
+        if t0[i] - s0 > 5.0:
+            late.append(t0[i])
+if late:
+    other = tag != kc_tag
+    cnt = {nm: 0 for nm in names.values()}
+    for x in late:
+        m = other & (t0 < x) & (t1 > x - 1.0)
+        for tg in set(tag[m].tolist()):
+            cnt[names.get(tg, str(tg))] += 1
+    print(f"{len(late)} KC blocks started >5 us late; blocks of other kernels ending at that moment:", cnt)
