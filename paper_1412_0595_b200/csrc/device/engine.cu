@@ -183,7 +183,7 @@ bool kernel_attributes(const std::string& name, int& regs, int& sharedBytes, int
 
 // ---------------------------------------------------------------------------
 
-using ChainFn = void (*)(ssbk::GroupDev, float*, long long, int, int);
+using ChainFn = void (*)(ssbk::GroupDev, float*, long long, int, int, int);
 template <int... NP>
 constexpr std::array<ChainFn, sizeof...(NP)> chain_table(std::integer_sequence<int, NP...>) {
     return {ssbk::dense_window_chain_kernel<4 * (NP + 1)>...};
@@ -341,6 +341,7 @@ struct DeviceEngine::Impl {
     std::string timelinePath;
     int prioHigh = 0;          // the device's greatest launch priority
     bool usePdl = false;       // SSB_PDL=1: programmatic launch of consecutive updates
+    int chainBlocks = 0;       // SSB_CHAIN_BLOCKS: persistent chain-gather grid (0: a block per step)
     bool usePriority = true;   // SSB_PRIORITY=0 disables the update priority
     std::string tracePath;  // SSB_TRACE: per-block records written at release
     unsigned long long* traceBuf = nullptr;
@@ -473,8 +474,9 @@ struct DeviceEngine::Impl {
             const int smem = ssbk::kChainStages * ssbk::kChainPer *
                              (ssbk::kChainCopiers / (G.nPost / 4)) * G.nPost * 4;
             launch(std::string(tag) + gname, [&] {
-                chain_kernel(G.nPost)<<<dim3(1, nW), chain_threads(G.nPost), smem, s>>>(G, out, stride,
-                                                                                   wLo, first);
+                const int gy = chainBlocks > 0 ? std::min(nW, chainBlocks) : nW;
+                chain_kernel(G.nPost)<<<dim3(1, gy), chain_threads(G.nPost), smem, s>>>(
+                    G, out, stride, wLo, nW, first);
             });
         } else if (G.nPost % 4 == 0 && !usePipe) {
             dim3 grid((G.nPost + ssbk::kWarpSlab - 1) / ssbk::kWarpSlab, nW);
@@ -1000,6 +1002,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     CK(cudaDeviceGetStreamPriorityRange(&leastPrio, &prioHigh));
     usePriority = !std::getenv("SSB_PRIORITY") || std::string(std::getenv("SSB_PRIORITY")) != "0";
     usePdl = std::getenv("SSB_PDL") && std::string(std::getenv("SSB_PDL")) == "1";
+    if (const char* e = std::getenv("SSB_CHAIN_BLOCKS")) chainBlocks = std::atoi(e);
     for (auto& s : auxStreams) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
 
     // kernels with large dynamic shared tiles (the limit is per function and
