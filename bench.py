@@ -394,8 +394,10 @@ def main():
     if not args.no_e2e:
         k_e2e = 4
         spec_e = make_spec(k_e2e + 1.0, seed=11)
+        # 512 MB of pinned host memory for the raster drains (allocated at
+        # construction, untimed): each step's ~59 MB copies straight into it
         sim_e = S.Simulation(spec_e, S.StorageMode.FromSpec,
-                             S.EngineOptions(device=dev, window=args.window))
+                             S.EngineOptions(device=dev, window=args.window, rasterPinnedMB=512))
         sim_e.step(STEPS_PER_SIM_SECOND)
         held = sim_e.drain_raster()
         c0 = sim_e.spike_counts()
@@ -427,10 +429,10 @@ def main():
         e2e = {"value": statistics.median(vals), "unit": UNIT, "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": int(statistics.median(d2h)),
                "what": "4 bench steps of ssb_step(10,000), each step's raster events moved "
-                       "to host memory (ssb_raster_drain_async, overlapping the next step; "
-                       "the final ssb_raster_drain inside the timed region), wall clock; "
-                       "network uploaded once at construction (untimed, as in the "
-                       "reference arm)",
+                       "to host memory (ssb_raster_drain_async into the engine's pinned "
+                       "raster pool, overlapping the next step; the final ssb_raster_drain "
+                       "inside the timed region), wall clock; network uploaded and pool "
+                       "pinned once at construction (untimed, as in the reference arm)",
                "with_build": {"value": max(wb), "what": "ssb_create (host build + upload) + "
                               "10,000 steps + ssb_finish, wall clock, best of 2"}}
 

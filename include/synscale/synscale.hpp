@@ -333,6 +333,7 @@ struct EngineOptions {
     int rank = 0, world = 1, virtualWorld = 0, shardMinSize = 0;
     bool hasCommId = false;
     std::array<unsigned char, 128> commId{};
+    int rasterPinnedMB = 0;  // pinned host pool for raster drains (B200 extension)
 };
 
 // NCCL unique id for EngineOptions::commId (B200 extension).

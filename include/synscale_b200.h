@@ -157,6 +157,10 @@ typedef struct ssb_engine_opts {
     int32_t shard_min_size;      /* 0 = default (64) */
     int32_t has_comm_id;
     uint8_t comm_id[128];
+    /* pinned host memory (MB) allocated at creation for raster drains: a
+     * drain that fits copies straight into it at PCIe speed (0 = none:
+     * drains go through pinned staging into pageable memory) */
+    int32_t raster_pinned_mb;
 } ssb_engine_opts;
 
 /* Result summary (RunResult, engine.hpp:35-42). */

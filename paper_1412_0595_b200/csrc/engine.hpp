@@ -83,6 +83,7 @@ struct EngineConfig {
     int shardMinSize = 64;  // CondLif populations at least this large are split
     bool hasCommId = false;
     std::array<unsigned char, 128> commId{};
+    int rasterPinnedMB = 0;  // pinned host pool for raster drains (0 = none)
 };
 
 // Which populations a world of R ranks splits, and where (host, no CUDA).

@@ -245,6 +245,7 @@ ssb::EngineConfig to_config(const ssb_engine_opts* o) {
     if (o->shard_min_size > 0) c.shardMinSize = o->shard_min_size;
     c.hasCommId = o->has_comm_id != 0;
     std::memcpy(c.commId.data(), o->comm_id, 128);
+    c.rasterPinnedMB = std::max(0, static_cast<int>(o->raster_pinned_mb));
     return c;
 }
 

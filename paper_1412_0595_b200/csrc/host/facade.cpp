@@ -26,6 +26,7 @@ ssb::EngineConfig to_config(const EngineOptions& o) {
     if (o.shardMinSize > 0) c.shardMinSize = o.shardMinSize;
     c.hasCommId = o.hasCommId;
     c.commId = o.commId;
+    c.rasterPinnedMB = std::max(0, o.rasterPinnedMB);
     return c;
 }
 

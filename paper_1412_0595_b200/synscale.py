@@ -404,6 +404,9 @@ class EngineOptions:
     virtualWorld: int = 0
     shardMinSize: int = 0
     commId: Optional[bytes] = None
+    # pinned host memory (MB) allocated at creation for raster drains: a drain
+    # that fits copies straight into it at PCIe speed (0 = staged drains)
+    rasterPinnedMB: int = 0
 
     def to_c(self) -> L.ssb_engine_opts:
         o = L.ssb_engine_opts()
@@ -422,6 +425,7 @@ class EngineOptions:
         o.rank = self.rank
         o.world_size = max(1, self.world)
         o.virtual_world = self.virtualWorld
+        o.raster_pinned_mb = max(0, self.rasterPinnedMB)
         if self.shardMinSize:
             o.shard_min_size = self.shardMinSize
         if self.commId is not None:

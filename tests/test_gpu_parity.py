@@ -449,6 +449,24 @@ def test_raster_drain_midway_keeps_results(golden):
         golden["runs"]["cfg2_100ms"]["raster_sha"]
 
 
+def test_raster_pinned_pool_drains_keep_results(golden):
+    """EngineOptions.rasterPinnedMB: drains that fit copy straight into pinned
+    pool blocks, the rest (pool exhausted: one 32 MB block, held by the first
+    drain's chunk) go through staging; async and waited drains interleave and
+    the finished raster is the golden one."""
+    spec, mode = GOLDEN["cfg2_100ms"]()
+    sim = gpu_sim(spec, mode, window=64, rasterPinnedMB=32)
+    sim.step(200)
+    sim.drain_raster(wait=False)  # takes the pool's only block
+    sim.step(300)
+    assert sim.drain_raster() > 0  # staged: the pool is empty
+    sim.step(250)
+    sim.drain_raster(wait=False)
+    r = sim.finish()
+    assert specs.sha(r.raster.step, r.raster.population, r.raster.neuron) == \
+        golden["runs"]["cfg2_100ms"]["raster_sha"]
+
+
 def test_nccl_exchange_selftest():
     """The split engine's collectives (dlopen'd libnccl, one-rank communicator):
     all-gather and sum, plain and captured in a CUDA graph."""
