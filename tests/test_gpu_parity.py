@@ -194,6 +194,34 @@ def test_fault_injection_spreads_like_reference(oracle_mod):
     assert rg.sumNaNs == o.sum_nans() and rg.sumNaNs > 0
 
 
+def test_division_edge_numerators_rerun_exactly(oracle_mod):
+    """The window kernels divide (eLeak - v) / tauM without a branch and rerun a
+    chunk exactly when a numerator left the fast path's range: tiny, huge,
+    infinite and NaN numerators written into a population's v (eLeak = 0, so
+    v = 1e-35 gives a subnormal-range numerator) match the oracle step by step."""
+    spec = specs.mbody_spec(1000, 0.5, 6.0)
+    kc = spec.populations[spec.pop_index("kc")]
+    kc.params.eLeakMV = 0.0
+    kc.params.vResetMV = 0.0
+    kc.params.vThreshMV = 15.0
+    kc.params.eExcMV = 60.0
+    for window in (1, 16):
+        g = gpu_sim(spec, window=window)
+        o = cpu_sim(oracle_mod, spec)
+        g.step(5)
+        o.step(5)
+        v = o.state(2, "v")
+        v[0], v[1], v[2], v[3], v[40] = 1e-35, -3e-38, 1e36, np.inf, np.nan
+        g.push(2, "v", v)
+        o.set_state(2, "v", v)
+        for k in range(6):
+            g.step(3)
+            o.step(3)
+            assert_state_equal(g, o, spec, f"window {window} after {5 + 3 * (k + 1)} steps")
+        rg, ro = g.finish(), o.finish()
+        assert np.array_equal(rg.raster.neuron, ro[2])
+
+
 def test_storage_modes_and_windows_do_not_change_results():
     """test_engine.cpp:455-474 plus the engine's own window/graph knobs."""
     spec = specs.mbody_spec(2000, 0.2, 200.0)
