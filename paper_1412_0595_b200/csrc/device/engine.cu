@@ -805,6 +805,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         d.eExc = hp.eExc;
         d.eInh = hp.eInh;
         d.vThresh = hp.vThresh;
+        d.halves = !(std::getenv("SSB_HALVES") && std::string(std::getenv("SSB_HALVES")) == "0");
         d.vReset = hp.vReset;
         d.synDecay = hp.synDecay;
         d.dt = net.dtS;
