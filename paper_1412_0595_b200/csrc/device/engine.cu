@@ -700,6 +700,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     // accumulator plans
     pops.resize(nPops);
     reservedSMs = nPops > 1 && !stepMode ? std::max(4, smCount / 10) : 0;
+    if (const char* e = std::getenv("SSB_RESERVED_SMS")) reservedSMs = std::atoi(e);
     for (int gi = 0; gi < static_cast<int>(net.groups.size()); ++gi) {
         const auto& g = net.groups[gi];
         pops[g.post].accGroups[g.inhibitory ? 1 : 0].push_back(gi);
