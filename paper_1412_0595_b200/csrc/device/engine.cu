@@ -772,10 +772,20 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     {
         // The host runs at most kRing launches ahead of the last cursor it has
         // seen, so the arena must hold kRing + 1 launches of worst-case events
-        // (every neuron spiking every step); beyond 4G events (16 GB per arena,
-        // two arenas) shrink the launch.
+        // (every neuron spiking every step).  The two arenas may take 4G events
+        // each or 30% of the device memory free now, whichever is more (a
+        // split world's every rank records the global raster: at 8 x 100k KC
+        // a 4G cap allowed 6 windows per launch and each graph boundary cost
+        // ~100 us per window); beyond that the launch shrinks.
+        std::size_t freeB = 0, totalB = 0;
+        if (cudaMemGetInfo(&freeB, &totalB) != cudaSuccess) {
+            cudaGetLastError();
+            freeB = 0;
+        }
+        const std::int64_t budget = std::max<std::int64_t>(
+            std::int64_t(1) << 32, static_cast<std::int64_t>(0.30 * static_cast<double>(freeB)) / 8);
         const std::int64_t perWin = static_cast<std::int64_t>(Wmax) * totalNeurons;
-        const std::int64_t fit = (std::int64_t(1) << 32) / ((kRing + 1) * std::max<std::int64_t>(perWin, 1));
+        const std::int64_t fit = budget / ((kRing + 1) * std::max<std::int64_t>(perWin, 1));
         graphWindows = static_cast<int>(std::clamp<std::int64_t>(fit, 1, graphWindows));
     }
     nSets = std::clamp(graphWindows, 2, kMaxSets);
