@@ -61,7 +61,8 @@ def scaling_config(mode, world, fallback=None):
     if mode == "split":
         return {"parallelism": f"split{world}", "n_kc_total": N_KC * world,
                 "split": "KC and DN by neuron ranges, PN/LHI replicated, per-window NCCL "
-                         "all-gather of spike bitmasks"}
+                         "all-gather of spike bitmasks; each rank records its own neurons' "
+                         "spikes (rank 0 also PN/LHI), events summed over ranks"}
     if mode == "replicas":
         cfg = {"parallelism": f"replicas{world}", "replicas": world}
         if fallback:
@@ -302,8 +303,10 @@ def main():
             spec = specs.mbody_spec(N_KC * world, FRAC, total_s * 1000.0, seed=7)
             cid = [S.comm_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(cid, src=0)
+            # each rank records its own neurons (rank 0 also PN / LHI): the
+            # raster and the spike counts are the sums over ranks
             opts = S.EngineOptions(device=dev, window=args.window, world=world, rank=rank,
-                                   commId=cid[0])
+                                   commId=cid[0], rasterLocal=True)
         else:
             spec = make_spec(total_s, seed=7 + rank)
             opts = S.EngineOptions(device=dev, window=args.window)
@@ -367,8 +370,9 @@ def main():
         tt = torch.tensor([t_local], device=f"cuda:{dev}", dtype=torch.float64)
         ee = torch.tensor([ev_local], device=f"cuda:{dev}", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        if mode == "replicas":  # independent networks: add them up
-            dist.all_reduce(ee, op=dist.ReduceOp.SUM)
+        # replicas: independent networks; split: each rank counted its own
+        # neurons' spikes (local raster) -- either way the sum over ranks
+        dist.all_reduce(ee, op=dist.ReduceOp.SUM)
         t_max, ev_sum = float(tt.item()), float(ee.item())
     value = ev_sum / t_max
     sim_seconds = args.steps

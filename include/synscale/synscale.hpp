@@ -334,6 +334,7 @@ struct EngineOptions {
     bool hasCommId = false;
     std::array<unsigned char, 128> commId{};
     int rasterPinnedMB = 0;  // pinned host pool for raster drains (B200 extension)
+    bool rasterLocal = false;  // split runs: each rank records its own neurons only
 };
 
 // NCCL unique id for EngineOptions::commId (B200 extension).

@@ -161,6 +161,12 @@ typedef struct ssb_engine_opts {
      * drain that fits copies straight into it at PCIe speed (0 = none:
      * drains go through pinned staging into pageable memory) */
     int32_t raster_pinned_mb;
+    /* split runs (world_size > 1, not virtual_world): 1 = each rank records
+     * only its own neurons of split populations, and rank 0 alone the whole
+     * (replicated) ones; the global raster is the union over ranks (spike
+     * counts likewise sum over ranks).  0 = every rank records the global
+     * raster. */
+    int32_t raster_local;
 } ssb_engine_opts;
 
 /* Result summary (RunResult, engine.hpp:35-42). */

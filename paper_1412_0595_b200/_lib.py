@@ -81,6 +81,7 @@ class ssb_engine_opts(C.Structure):
         ("rank", C.c_int32), ("world_size", C.c_int32), ("virtual_world", C.c_int32),
         ("shard_min_size", C.c_int32), ("has_comm_id", C.c_int32),
         ("comm_id", C.c_uint8 * 128), ("raster_pinned_mb", C.c_int32),
+        ("raster_local", C.c_int32),
     ]
 
 

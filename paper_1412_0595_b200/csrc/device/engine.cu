@@ -239,6 +239,7 @@ struct DeviceEngine::Impl {
     int world = 1;              // ranks (or virtual shards) the network is split over
     bool virtualShard = false;  // one of several shards in this process (exchange by copies)
     bool emulateExchange = false;  // SSB_EMULATE_EXCHANGE diagnostic (see the constructor)
+    bool rasterLocal = false;      // split run recording this rank's neurons only
     bool serial = false;        // one stream, no graphs (profiling, virtual shards)
     bool ownsStream = true;
     std::unique_ptr<Comm> comm;  // NCCL, one process per GPU
@@ -718,7 +719,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         P.nwGlobal = (P.nGlobal + 31) / 32;
         // kernel-side bitmask stride: a split population sends equal slices
         P.nwords = P.sharded ? (hp.chunk + 31) / 32 : (hp.n + 31) / 32;
-        totalNeurons += P.nGlobal;
+        // events a window can record: a local raster holds this rank's part
+        totalNeurons += !rasterLocal ? P.nGlobal : P.sharded ? P.n : cfg.rank == 0 ? P.nGlobal : 0;
         for (int a = 0; a < 2; ++a) {
             auto& A = P.acc[a];
             const auto& gl = P.accGroups[a];
@@ -988,11 +990,26 @@ void DeviceEngine::Impl::build(const HostNet& net) {
 
     // raster arena
     raster.nPops = nPops;
-    for (int pi = 0; pi < nPops; ++pi) {
-        raster.n[pi] = pops[pi].nGlobal;
-        raster.count[pi] = pops[pi].dev.count;
-        raster.list[pi] = pops[pi].dev.list;
-    }
+    // a local raster reads a split population's local lists (indices + lo) and
+    // on ranks other than 0 records nothing of the replicated ones
+    int* zeroCounts = rasterLocal ? alloc<int>(static_cast<std::size_t>(Wmax)) : nullptr;
+    auto raster_src = [&](ssbk::RasterDev& r, int pi, int b) {
+        const auto& P = pops[pi];
+        r.n[pi] = P.nGlobal;
+        r.add[pi] = 0;
+        r.count[pi] = P.devb[b].count;
+        r.list[pi] = P.devb[b].list;
+        if (!rasterLocal) return;
+        if (P.sharded) {
+            r.n[pi] = P.n;
+            r.add[pi] = P.lo;
+            r.count[pi] = P.kdev[b].count;
+            r.list[pi] = P.kdev[b].list;
+        } else if (cfg.rank != 0) {
+            r.count[pi] = zeroCounts;
+        }
+    };
+    for (int pi = 0; pi < nPops; ++pi) raster_src(raster, pi, 0);
     // raster arena capacity for kRing + 1 launches of worst-case events
     const std::int64_t perWindow = static_cast<std::int64_t>(Wmax) * totalNeurons;
     const std::int64_t perLaunch = perWindow * graphWindows;
@@ -1027,10 +1044,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     raster.doneCounter = alloc<unsigned>(1);
     for (int b = 0; b < nSets; ++b) {
         rasterb[b] = raster;
-        for (int pi = 0; pi < nPops; ++pi) {
-            rasterb[b].count[pi] = pops[pi].devb[b].count;
-            rasterb[b].list[pi] = pops[pi].devb[b].list;
-        }
+        for (int pi = 0; pi < nPops; ++pi) raster_src(rasterb[b], pi, b);
     }
     // capture streams: one per population, one for deliver + raster
     // 3 per population, the raster's, then a second group stream per population
@@ -1168,7 +1182,7 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
         if (wide) after_wide(sm);
         edge(sm, sp);
         launchStream = sp;
-        if (P.grid > 1 && !P.sharded) {
+        if (P.grid > 1 && (!P.sharded || rasterLocal)) {  // (split: the local raster's lists)
             const int bs = std::min(1024, round_up((P.nwords + ssbk::kCompactK - 1) / ssbk::kCompactK, 32));
             launch("compact_window:" + P.name, [&] {
                 ssbk::compact_window_kernel<<<W, bs, 0, sp>>>(K.bits, P.nwords, P.n, K.list, K.count);
@@ -1494,6 +1508,7 @@ DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfgIn)
         m.world = R;
         m.smCount = smCount;
         m.virtualShard = virt;
+        m.rasterLocal = cfg.rasterLocal && split && !virt;
         m.emulateExchange = emulate;
         if (virt) {  // lockstep across shards on one stream
             m.serial = true;

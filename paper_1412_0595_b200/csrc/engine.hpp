@@ -84,6 +84,7 @@ struct EngineConfig {
     bool hasCommId = false;
     std::array<unsigned char, 128> commId{};
     int rasterPinnedMB = 0;  // pinned host pool for raster drains (0 = none)
+    bool rasterLocal = false;  // split runs: record this rank's neurons only (see the C ABI)
 };
 
 // Which populations a world of R ranks splits, and where (host, no CUDA).

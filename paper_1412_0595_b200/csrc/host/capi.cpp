@@ -246,6 +246,7 @@ ssb::EngineConfig to_config(const ssb_engine_opts* o) {
     c.hasCommId = o->has_comm_id != 0;
     std::memcpy(c.commId.data(), o->comm_id, 128);
     c.rasterPinnedMB = std::max(0, static_cast<int>(o->raster_pinned_mb));
+    c.rasterLocal = o->raster_local != 0;
     return c;
 }
 

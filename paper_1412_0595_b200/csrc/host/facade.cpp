@@ -27,6 +27,7 @@ ssb::EngineConfig to_config(const EngineOptions& o) {
     c.hasCommId = o.hasCommId;
     c.commId = o.commId;
     c.rasterPinnedMB = std::max(0, o.rasterPinnedMB);
+    c.rasterLocal = o.rasterLocal;
     return c;
 }
 

@@ -407,6 +407,9 @@ class EngineOptions:
     # pinned host memory (MB) allocated at creation for raster drains: a drain
     # that fits copies straight into it at PCIe speed (0 = staged drains)
     rasterPinnedMB: int = 0
+    # split runs: each rank records only its own neurons (rank 0 also the
+    # replicated populations); the raster and spike counts sum over ranks
+    rasterLocal: bool = False
 
     def to_c(self) -> L.ssb_engine_opts:
         o = L.ssb_engine_opts()
@@ -426,6 +429,7 @@ class EngineOptions:
         o.world_size = max(1, self.world)
         o.virtual_world = self.virtualWorld
         o.raster_pinned_mb = max(0, self.rasterPinnedMB)
+        o.raster_local = 1 if self.rasterLocal else 0
         if self.shardMinSize:
             o.shard_min_size = self.shardMinSize
         if self.commId is not None:

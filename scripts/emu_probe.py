@@ -13,7 +13,8 @@ from paper_1412_0595_b200 import synscale as S  # noqa: E402
 R = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 spec = specs.mbody_spec(100_000 * R, 0.05, 300.0)
 sim = S.Simulation(spec, S.StorageMode.FromSpec,
-                   S.EngineOptions(window=256, world=R, rank=R // 2, profile=True))
+                   S.EngineOptions(window=256, world=R, rank=R // 2, profile=True,
+                                   rasterLocal=os.environ.get("EMU_LOCAL", "1") == "1"))
 sim.step(256)
 sim.sync()
 sim.reset_kernel_stats()

@@ -22,7 +22,7 @@ if len(sys.argv) > 1:  # child: one M
     if emu > 1:
         os.environ["SSB_EMULATE_EXCHANGE"] = "1"
         spec, mode = specs.mbody_spec(100_000 * emu, 0.05, (n * 2 + 512) * 0.1), S.StorageMode.FromSpec
-        extra = {"world": emu, "rank": emu // 2}
+        extra = {"world": emu, "rank": emu // 2, "rasterLocal": os.environ.get("GS_LOCAL", "1") == "1"}
     else:
         spec, mode = specs.config_spec(3, (n * 2 + 512) * 0.1)
         split = os.environ.get("GS_SPLIT") == "1"

@@ -22,7 +22,8 @@ emu = int(os.environ.get("TR_EMULATE", "0"))
 if emu > 1:
     os.environ["SSB_EMULATE_EXCHANGE"] = "1"
     spec, mode = specs.mbody_spec(100_000 * emu, 0.05, (nwin + 40) * 25.6), S.StorageMode.FromSpec
-    sim = S.Simulation(spec, mode, S.EngineOptions(window=256, world=emu, rank=emu // 2))
+    sim = S.Simulation(spec, mode, S.EngineOptions(window=256, world=emu, rank=emu // 2,
+                                                   rasterLocal=True))
 else:
     spec, mode = specs.config_spec(3, (nwin + 40) * 25.6)
     sim = S.Simulation(spec, mode, S.EngineOptions(window=256))

@@ -526,14 +526,17 @@ def test_sweep_cells_match_oracle(oracle_mod):
 
 
 @pytest.mark.parametrize("name", ["cfg3_20ms", "cfg2_100ms", "izh_ff_200ms"])
-def test_nccl_split_path_one_rank_matches_golden(golden, name):
+@pytest.mark.parametrize("local", [False, True])
+def test_nccl_split_path_one_rank_matches_golden(golden, name, local):
     """A communicator id with a world of one rank runs the whole split path on
     a real (one-rank) NCCL communicator: per-window all-gathers captured in the
-    window graphs, assembly, compaction, gathered state pulls and the NaN sum."""
+    window graphs, assembly, compaction, gathered state pulls and the NaN sum;
+    with rasterLocal the raster comes from the rank's own lists (the local
+    compaction and index offset of split populations; one rank owns all)."""
     spec, mode = GOLDEN[name]()
     g = golden["runs"][name]
     sim = gpu_sim(spec, mode, window=64, world=1, rank=0, commId=S.comm_unique_id(),
-                  shardMinSize=32)
+                  shardMinSize=32, rasterLocal=local)
     r = sim.finish()
     assert specs.sha(r.raster.step, r.raster.population, r.raster.neuron) == g["raster_sha"]
     assert r.sumNaNs == g["sum_nans"]
