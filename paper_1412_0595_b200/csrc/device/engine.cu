@@ -1191,7 +1191,9 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
     } else {
         edge(sm, sp);
     }
-    if (P.sharded) {
+    // a split population's global spikes are needed by its consumers and a
+    // global raster; a local raster of a sink population (DN) needs none
+    if (P.sharded && (!rasterLocal || !P.consumers.empty())) {
         // the window's exchange: every rank's local bits, in rank order
         if (comm) {
             // collectives of one communicator must run in the same order on
