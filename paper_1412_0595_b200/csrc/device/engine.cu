@@ -227,7 +227,8 @@ struct DeviceEngine::Impl {
         bool sharded = false;
         int nGlobal = 0, lo = 0, shardChunk = 0, nwGlobal = 0;
         ssbk::PopDev kdev[kMaxSets]{};
-        uint32_t* gathered[kMaxSets] = {};  // [world][W][nwords]
+        uint32_t* gathered[kMaxSets] = {};  // [world][exchange words]
+        bool rankCounts = false;            // exchange carries per-step counts (see build)
     };
     struct LaunchStat {
         std::string name;
@@ -425,6 +426,12 @@ struct DeviceEngine::Impl {
         CK(cudaStreamWaitEvent(to, e, 0));
     }
     void assemble_compact(int pi, int W, int b, cudaStream_t s);
+    // words a split population's rank sends per window: its local bits, plus
+    // its per-step counts when the global lists are assembled per rank slice
+    std::size_t exchange_words(const PopRt& P, int W = 0) const {
+        return P.rankCounts ? static_cast<std::size_t>(Wmax) * P.nwords + Wmax
+                            : static_cast<std::size_t>(W > 0 ? W : Wmax) * P.nwords;
+    }
     std::int64_t pre_launch(int W, int M);
     void post_launch(int W, int M, std::int64_t add);
     void enqueue_tail(int W, int b, cudaStream_t s);
@@ -894,8 +901,18 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         }
         if (P.sharded) {
             const std::size_t ng = static_cast<std::size_t>(P.nGlobal);
+            // ranks owning whole words send their per-step counts with their
+            // bits (local bits then counts in one buffer), so the global lists
+            // are assembled rank slice by rank slice
+            P.rankCounts = P.nwGlobal > 32 && P.shardChunk % 32 == 0;
+            const std::size_t exw = exchange_words(P);
             for (int b = 0; b < nSets; ++b) {
-                P.gathered[b] = alloc<uint32_t>(static_cast<std::size_t>(world) * Wmax * P.nwords);
+                if (P.rankCounts) {
+                    uint32_t* lb = alloc<uint32_t>(exw);
+                    P.kdev[b].bits = lb;
+                    P.kdev[b].count = reinterpret_cast<int*>(lb + static_cast<std::size_t>(Wmax) * P.nwords);
+                }
+                P.gathered[b] = alloc<uint32_t>(static_cast<std::size_t>(world) * exw);
                 auto& g = P.devb[b];
                 g.n = P.nGlobal;
                 g.nwords = P.nwGlobal;
@@ -1182,7 +1199,8 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
         if (wide) after_wide(sm);
         edge(sm, sp);
         launchStream = sp;
-        if (P.grid > 1 && (!P.sharded || rasterLocal)) {  // (split: the local raster's lists)
+        // (split: the local raster's lists, or the counts the exchange carries)
+        if (P.grid > 1 && (!P.sharded || rasterLocal || P.rankCounts)) {
             const int bs = std::min(1024, round_up((P.nwords + ssbk::kCompactK - 1) / ssbk::kCompactK, 32));
             launch("compact_window:" + P.name, [&] {
                 ssbk::compact_window_kernel<<<W, bs, 0, sp>>>(K.bits, P.nwords, P.n, K.list, K.count);
@@ -1200,14 +1218,13 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
             // every rank: chain them (the enqueue order is identical on all
             // ranks; independent streams could otherwise reorder them)
             if (multiStream && lastCollective) CK(cudaStreamWaitEvent(sp, lastCollective, 0));
-            comm->allgather_u32(P.kdev[b].bits, P.gathered[b],
-                                static_cast<std::size_t>(W) * P.nwords, sp);
+            comm->allgather_u32(P.kdev[b].bits, P.gathered[b], exchange_words(P, W), sp);
             if (multiStream) {
                 lastCollective = capture_event();
                 CK(cudaEventRecord(lastCollective, sp));
             }
         } else if (emulateExchange) {
-            const std::size_t bytes = static_cast<std::size_t>(W) * P.nwords * 4;
+            const std::size_t bytes = exchange_words(P, W) * 4;
             for (int r = 0; r < world; ++r)
                 CK(cudaMemcpyAsync(reinterpret_cast<char*>(P.gathered[b]) + r * bytes,
                                    P.kdev[b].bits, bytes, cudaMemcpyDeviceToDevice, sp));
@@ -1227,6 +1244,14 @@ void DeviceEngine::Impl::assemble_compact(int pi, int W, int b, cudaStream_t s) 
             ssbk::assemble_compact_small_kernel<<<W, 32 * P.nwGlobal, 0, s>>>(
                 P.gathered[b], W, P.nwords, P.shardChunk, P.nGlobal, P.nwGlobal, D.bits, D.list,
                 D.count);
+        });
+        return;
+    }
+    if (P.rankCounts) {
+        const int bsr = std::min(1024, round_up((P.nwords + ssbk::kCompactK - 1) / ssbk::kCompactK, 32));
+        launch("assemble_compact:" + P.name, [&] {
+            ssbk::assemble_compact_ranks_kernel<<<dim3(W, world), bsr, 0, s>>>(
+                P.gathered[b], Wmax, P.nwords, P.nwGlobal, P.nGlobal, D.bits, D.list, D.count);
         });
         return;
     }
@@ -1570,7 +1595,7 @@ void DeviceEngine::lockstep(int W) {
     for (int pi : m0.order) {
         for (auto* m : all) m->enqueue_pop(pi, W, b, m0.stream);
         if (!m0.pops[pi].sharded) continue;
-        const std::size_t words = static_cast<std::size_t>(W) * m0.pops[pi].nwords;
+        const std::size_t words = m0.exchange_words(m0.pops[pi], W);
         for (int src = 0; src < R; ++src)
             for (int dst = 0; dst < R; ++dst)
                 CK(cudaMemcpyAsync(all[dst]->pops[pi].gathered[b] + src * words,
