@@ -185,16 +185,20 @@ bool kernel_attributes(const std::string& name, int& regs, int& sharedBytes, int
 // ---------------------------------------------------------------------------
 
 using ChainFn = void (*)(ssbk::GroupDev, float*, long long, int, int, int);
+// steps a chain block folds side by side (its stage rows <= 32 floats wide)
+constexpr int chain_steps(int nPost) { return nPost <= 8 ? 4 : nPost <= 16 ? 2 : 1; }
 template <int... NP>
 constexpr std::array<ChainFn, sizeof...(NP)> chain_table(std::integer_sequence<int, NP...>) {
-    return {ssbk::dense_window_chain_kernel<4 * (NP + 1)>...};
+    return {ssbk::dense_window_chain_kernel<4 * (NP + 1), chain_steps(4 * (NP + 1))>...};
 }
 ChainFn chain_kernel(int nPost) {  // nPost % 4 == 0, <= kChainMaxPost
     static constexpr auto k =
         chain_table(std::make_integer_sequence<int, ssbk::kChainMaxPost / 4>{});
     return k[nPost / 4 - 1];
 }
-int chain_threads(int nPost) { return ssbk::kChainCopiers + 32 * ((nPost + 31) / 32); }
+int chain_threads(int nPost) {
+    return ssbk::kChainCopiers + 32 * ((nPost * chain_steps(nPost) + 31) / 32);
+}
 
 struct DeviceEngine::Impl {
     // window-buffer sets: every window of a graph launch gets its own set of
@@ -493,10 +497,12 @@ struct DeviceEngine::Impl {
     void launch_dense(const ssbk::GroupDev& G, const std::string& gname, const char* tag,
                       float* out, long long stride, int wLo, int nW, int first, cudaStream_t s) {
         if (G.nPost % 4 == 0 && G.nPost <= ssbk::kChainMaxPost && !usePipe) {
-            const int smem = ssbk::kChainStages * ssbk::kChainPer *
-                             (ssbk::kChainCopiers / (G.nPost / 4)) * G.nPost * 4;
+            const int cw = G.nPost * chain_steps(G.nPost);  // stage row width
+            const int smem = ssbk::kChainStages * ssbk::kChainPer * (ssbk::kChainCopiers / (cw / 4)) *
+                             cw * 4;
             launch(std::string(tag) + gname, [&] {
-                const int gy = chainBlocks > 0 ? std::min(nW, chainBlocks) : nW;
+                const int groups = (nW + chain_steps(G.nPost) - 1) / chain_steps(G.nPost);
+                const int gy = chainBlocks > 0 ? std::min(groups, chainBlocks) : groups;
                 chain_kernel(G.nPost)<<<dim3(1, gy), chain_threads(G.nPost), smem, s>>>(
                     G, out, stride, wLo, nW, first);
             });
