@@ -39,6 +39,8 @@ t0, t1 = (t0 - base) / 1e3, (t1 - base) / 1e3  # us
 nkc = 100_000 * max(1, emu) // max(1, emu) if emu <= 1 else None
 kc_tag = max(int(x) for x in set(tag.tolist()) if x < 0xfffffff0)
 names = {kc_tag: "kc", 20: "lhi", 100: "dn", 0xffffffff: "kc_dn", 0xfffffffd: "raster"}
+if emu > 1:
+    names[16] = "dn (local slice)"
 # the last nwin windows' KC launches: split KC blocks into launches by start gaps
 k = np.where(tag == kc_tag)[0]
 order = k[np.argsort(t0[k])]
@@ -79,5 +81,6 @@ if late:
     for x in late:
         m = other & (t0 < x) & (t1 > x - 1.0)
         for tg in set(tag[m].tolist()):
-            cnt[names.get(tg, str(tg))] += 1
+            nm = names.get(tg, f"pop of {tg}")
+            cnt[nm] = cnt.get(nm, 0) + 1
     print(f"{len(late)} KC blocks started >5 us late; blocks of other kernels ending at that moment:", cnt)
