@@ -157,6 +157,17 @@ enum class ModelKind { Izhikevich, PoissonSource, CondLif, TraubMiles };
 enum class SynapseSign { Excitatory, Inhibitory };
 enum class StorageKind { Dense, Sparse };
 
+// Extension F2 (not in the reference): pair-based STDP on a dense
+// all-to-all excitatory group.  After step t's propagation, with traces
+// decayed once (x *= decPlus, y *= decMinus): a spiking pre row takes
+// w -= aMinus * y[j] on every column, a spiking post column takes
+// w += aPlus * x[row] on every row, a touched w is clipped to [0, wMax];
+// then spiking rows / columns add 1 to their trace.  fp32, no FMA.
+struct StdpRule {
+    bool enabled = false;
+    double aPlus = 0.0, aMinus = 0.0, tauPlusMs = 20.0, tauMinusMs = 20.0, wMax = 0.0;
+};
+
 struct IzhikevichParams {
     std::vector<double> a, b, c, d;
     std::vector<double> noiseAmplitude;
@@ -215,6 +226,7 @@ struct SynapseGroupSpec {
     StorageKind storage = StorageKind::Sparse;
     std::int32_t preOffset = 0;
     std::int32_t preCount = -1;
+    StdpRule stdp;  // extension F2
 };
 
 struct NetworkSpec {

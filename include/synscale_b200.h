@@ -53,6 +53,11 @@ enum { SSB_MODEL_IZHIKEVICH = 0, SSB_MODEL_POISSON = 1, SSB_MODEL_CONDLIF = 2,
 enum { SSB_SIGN_EXC = 0, SSB_SIGN_INH = 1 };
 /* StorageKind (network.hpp:16) */
 enum { SSB_STORAGE_DENSE = 0, SSB_STORAGE_SPARSE = 1 };
+/* Synapse plasticity (extension F2: the reference has no
+ * learning).  STDP = pair-based spike-timing-dependent
+ * plasticity with exponential traces on a dense all-to-all excitatory group;
+ * the rule is stated in DESIGN.md §1 (row A22). */
+enum { SSB_PLASTICITY_NONE = 0, SSB_PLASTICITY_STDP = 1 };
 /* StorageMode (engine.hpp:18) */
 enum { SSB_MODE_FROM_SPEC = 0, SSB_MODE_FORCE_DENSE = 1, SSB_MODE_FORCE_SPARSE = 2 };
 /* WeightDist::Kind (matrix.hpp:15-16) */
@@ -103,6 +108,10 @@ typedef struct ssb_group_desc {
     int32_t storage; /* SSB_STORAGE_* */
     int32_t pre_offset;
     int32_t pre_count; /* -1 = rest of the population */
+    /* extension F2 (zero = static, as in the reference): SSB_PLASTICITY_* and
+     * the STDP constants (cast to fp32; trace decays float(exp(-dt/tau))) */
+    int32_t plasticity;
+    double stdp_a_plus, stdp_a_minus, stdp_tau_plus_ms, stdp_tau_minus_ms, stdp_w_max;
 } ssb_group_desc;
 
 /* NetworkSpec (network.hpp:72-80). */
@@ -335,6 +344,10 @@ SSB_API int ssb_push_state(ssb_sim* sim, int32_t pop, int32_t field, const void*
 SSB_API int ssb_group_info(const ssb_sim* sim, int32_t group, int32_t* storage, int32_t* n_pre,
                            int32_t* n_post, int64_t* nnz);
 SSB_API int ssb_group_dense(const ssb_sim* sim, int32_t group, float* w, int64_t n);
+/* Extension F2: the dense group's weights as they are now (a plastic group's
+ * learned weights, read from the device after the steps so far; a static
+ * group's are ssb_group_dense's).  n = n_pre * n_post. */
+SSB_API int ssb_group_weights(ssb_sim* sim, int32_t group, float* w, int64_t n);
 SSB_API int ssb_group_sparse(const ssb_sim* sim, int32_t group, float* g, int32_t* post_ind,
                              int64_t* row_start);
 /* Simulation::finish() (engine.cpp:385-401): runs the remaining steps and

@@ -211,6 +211,11 @@ typedef struct {
     int64_t* rowStart;
     int64_t nnz;
     int32_t* windowed;
+    /* extension F2: STDP (fp32 constants, traces) */
+    int plastic;
+    float aPlus, aMinus, decPlus, decMinus, wMax;
+    float *x, *y;
+    uint8_t* postSpk;
 } or_group;
 
 typedef struct {
@@ -369,6 +374,17 @@ OR_API or_sim* or_create(const ssb_net_desc* net, int mode, char* err, size_t er
                     : mode == SSB_MODE_FORCE_SPARSE ? 0
                                                     : d->storage == SSB_STORAGE_DENSE;
         g->dense = dense;
+        if (d->plasticity == SSB_PLASTICITY_STDP) { /* extension F2 (dense all-to-all) */
+            g->plastic = 1;
+            g->aPlus = (float)d->stdp_a_plus;
+            g->aMinus = (float)d->stdp_a_minus;
+            g->decPlus = (float)exp(-net->dt_ms / d->stdp_tau_plus_ms);
+            g->decMinus = (float)exp(-net->dt_ms / d->stdp_tau_minus_ms);
+            g->wMax = (float)d->stdp_w_max;
+            g->x = zalloc_f((size_t)g->nPre);
+            g->y = zalloc_f((size_t)g->nPost);
+            g->postSpk = (uint8_t*)calloc((size_t)g->nPost + 1, 1);
+        }
         if (dense) {
             g->W = base;
         } else { /* to_sparse (matrix.cpp:144-162) */
@@ -412,6 +428,7 @@ OR_API void or_destroy(or_sim* s) {
     for (int i = 0; i < s->ngroups; ++i) {
         or_group* g = &s->groups[i];
         free(g->W), free(g->g), free(g->ind), free(g->rowStart), free(g->windowed);
+        free(g->x), free(g->y), free(g->postSpk);
     }
     free(s->pops), free(s->groups), free(s->evStep), free(s->evPop), free(s->evNeuron);
     free(s);
@@ -583,6 +600,38 @@ static void or_record(or_sim* s, int64_t step, int32_t pop, int32_t neuron) {
     ++s->nev;
 }
 
+/* Extension F2 (NOT in the reference; parity vs this statement
+ * only): pair-based STDP on a dense all-to-all group, after the step's
+ * propagation.  xd = x[r]*decPlus, yd = y[j]*decMinus; a spiking (windowed)
+ * pre row r: w -= aMinus*yd on every column; a spiking post column j:
+ * w += aPlus*xd on every row; a touched w is clipped to [0, wMax]; then
+ * x[r] = xd (+1 if r spiked), y[j] = yd (+1 if j spiked).  Rows in
+ * ascending order; no FMA (-ffp-contract=off). */
+static void or_stdp_step(or_group* g, const or_pop* post, int32_t nw) {
+    memset(g->postSpk, 0, (size_t)g->nPost);
+    for (int k = 0; k < post->nspk; ++k) g->postSpk[post->spikes[k]] = 1;
+    int32_t w = 0; /* cursor into the ascending windowed pre spike list */
+    for (int32_t r = 0; r < g->nPre; ++r) {
+        const int pre = w < nw && g->windowed[w] == r;
+        if (pre) ++w;
+        const float xd = g->x[r] * g->decPlus;
+        const float dw = g->aPlus * xd;
+        float* row = g->W + (size_t)r * (size_t)g->nPost;
+        for (int32_t j = 0; j < g->nPost; ++j) {
+            if (!pre && !g->postSpk[j]) continue;
+            float v = row[j];
+            if (pre) v = v - g->aMinus * (g->y[j] * g->decMinus);
+            if (g->postSpk[j]) v = v + dw;
+            row[j] = fminf(fmaxf(v, 0.0f), g->wMax);
+        }
+        g->x[r] = pre ? xd + 1.0f : xd;
+    }
+    for (int32_t j = 0; j < g->nPost; ++j) {
+        const float yd = g->y[j] * g->decMinus;
+        g->y[j] = g->postSpk[j] ? yd + 1.0f : yd;
+    }
+}
+
 /* Simulation::step (engine.cpp:316-356) */
 static void or_step_one(or_sim* s) {
     for (int i = 0; i < s->npops; ++i) {
@@ -612,12 +661,14 @@ static void or_step_one(or_sim* s) {
             int32_t r = pre->spikes[k] - g->preOffset;
             if (r >= 0 && r < g->preCount) g->windowed[nw++] = r;
         }
-        if (!nw) continue;
         float* acc = g->inhibitory ? post->inhIn : post->excIn;
-        if (g->dense)
-            or_propagate_dense_impl(g->W, g->nPost, g->windowed, nw, acc);
-        else
-            or_propagate_crs_impl(g->g, g->ind, g->rowStart, g->windowed, nw, acc);
+        if (nw) {
+            if (g->dense)
+                or_propagate_dense_impl(g->W, g->nPost, g->windowed, nw, acc);
+            else
+                or_propagate_crs_impl(g->g, g->ind, g->rowStart, g->windowed, nw, acc);
+        }
+        if (g->plastic) or_stdp_step(g, post, nw);
     }
     ++s->done;
 }

@@ -39,6 +39,9 @@ class ssb_pop_desc(C.Structure):
     ]
 
 
+PLASTICITY_NONE, PLASTICITY_STDP = 0, 1
+
+
 class ssb_group_desc(C.Structure):
     _fields_ = [
         ("name", C.c_char_p), ("pre", C.c_char_p), ("post", C.c_char_p),
@@ -46,6 +49,10 @@ class ssb_group_desc(C.Structure):
         ("weight_lo", C.c_double), ("weight_hi", C.c_double), ("weight_value", C.c_double),
         ("g_scale", C.c_double), ("storage", C.c_int32), ("pre_offset", C.c_int32),
         ("pre_count", C.c_int32),
+        # extension F2 (STDP); zero = static, as in the reference
+        ("plasticity", C.c_int32), ("stdp_a_plus", C.c_double), ("stdp_a_minus", C.c_double),
+        ("stdp_tau_plus_ms", C.c_double), ("stdp_tau_minus_ms", C.c_double),
+        ("stdp_w_max", C.c_double),
     ]
 
 
@@ -163,6 +170,7 @@ _SIGNATURES = {
     "ssb_push_state": (C.c_int, [_vp, _i32, _i32, _vp, _i64]),
     "ssb_group_info": (C.c_int, [_vp, _i32, P(_i32), P(_i32), P(_i32), P(_i64)]),
     "ssb_group_dense": (C.c_int, [_vp, _i32, P(_f32), _i64]),
+    "ssb_group_weights": (C.c_int, [_vp, _i32, P(_f32), _i64]),
     "ssb_group_sparse": (C.c_int, [_vp, _i32, P(_f32), P(_i32), P(_i64)]),
     "ssb_finish": (C.c_int, [_vp, P(ssb_run_summary)]),
     "ssb_result_rates": (C.c_int, [_vp, P(_dbl), _i32]),

@@ -267,6 +267,12 @@ struct DeviceEngine::Impl {
     cudaStream_t stream = nullptr;
     std::vector<PopRt> pops;
     std::vector<HostGroup> groupMeta;  // sizes only (arrays cleared)
+    // extension F2: plastic groups (step mode), one device view per buffer set
+    struct StdpRt {
+        int gi = 0, grid = 1, smem = 0;
+        ssbk::StdpDev dev[kMaxSets]{};
+    };
+    std::vector<StdpRt> stdp;
     std::vector<ssbk::GroupDev> groupDev;
     std::vector<int> order;
     std::vector<void*> allocations;
@@ -703,7 +709,11 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         if (static_cast<int>(q.size()) != nPops) cyclic = true;
         order = cyclic ? std::vector<int>() : q;
     }
-    stepMode = cyclic || cfg.forceStepMode;
+    // a plastic group's weights change after every step: step mode (the
+    // window pipeline's lagged post updates would read stale weights)
+    bool plastic = false;
+    for (const auto& g : net.groups) plastic = plastic || g.plastic;
+    stepMode = cyclic || cfg.forceStepMode || plastic;
     if (stepMode) {
         order.resize(nPops);
         std::iota(order.begin(), order.end(), 0);
@@ -1010,6 +1020,41 @@ void DeviceEngine::Impl::build(const HostNet& net) {
                     P.accb[b][a].g[k] = G;
                 }
             }
+    for (std::size_t gi = 0; gi < net.groups.size(); ++gi) {
+        const auto& g = net.groups[gi];
+        if (!g.plastic) continue;
+        StdpRt L;
+        L.gi = static_cast<int>(gi);
+        L.smem = (g.nPost + (g.nPost + 31) / 32) * 4;
+        if (L.smem > 200 * 1024)
+            throw synscale::SpecError("plastic group '" + g.name + "': too many post neurons");
+        if (L.smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(ssbk::stdp_update_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem));
+        const int nGroups = (g.nPre + 31) / 32;
+        L.grid = std::max(1, std::min((nGroups + 7) / 8, 8 * smCount));
+        ssbk::StdpDev D{};
+        D.W = const_cast<float*>(groupDev[gi].W);
+        D.x = alloc<float>(static_cast<std::size_t>(g.nPre));
+        D.y = alloc<float>(static_cast<std::size_t>(g.nPost));
+        D.preFlag = alloc<uint32_t>(static_cast<std::size_t>(nGroups));
+        D.nPre = g.nPre;
+        D.nPost = g.nPost;
+        D.preOffset = g.preOffset;
+        D.aPlus = g.aPlus;
+        D.aMinus = g.aMinus;
+        D.decPlus = g.decPlus;
+        D.decMinus = g.decMinus;
+        D.wMax = g.wMax;
+        for (int b = 0; b < nSets; ++b) {
+            L.dev[b] = D;
+            L.dev[b].preList = pops[g.pre].devb[b].list;
+            L.dev[b].preCnt = pops[g.pre].devb[b].count;
+            L.dev[b].postList = pops[g.post].devb[b].list;
+            L.dev[b].postCnt = pops[g.post].devb[b].count;
+        }
+        stdp.push_back(L);
+    }
 
     // raster arena
     raster.nPops = nPops;
@@ -1294,6 +1339,16 @@ void DeviceEngine::Impl::enqueue_tail(int W, int b, cudaStream_t s) {
             }
         }
     }
+    // extension F2: learning after the step's propagation (step mode, W = 1)
+    for (const auto& L : stdp) {
+        const auto& D = L.dev[b];
+        const std::string& nm = groupMeta[L.gi].name;
+        launch("stdp_mark:" + nm, [&] { ssbk::stdp_mark_kernel<<<8, 256, 0, s>>>(D); });
+        launch("stdp_update:" + nm,
+               [&] { ssbk::stdp_update_kernel<<<L.grid, 256, L.smem, s>>>(D); });
+        launch("stdp_post_trace:" + nm,
+               [&] { ssbk::stdp_post_trace_kernel<<<1, 1024, 0, s>>>(D); });
+    }
     launch("raster_window", [&] {
         ssbk::raster_window_kernel<<<W * raster.nPops, 256, 0, s>>>(rasterb[b], W);
     });
@@ -1533,6 +1588,10 @@ DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfgIn)
     // a communicator id with a world of one rank still runs the split path
     // (exchange included) on a one-rank communicator
     const bool split = R > 1 || (!virt && cfg.hasCommId);
+    for (const auto& g : net.groups)
+        if (g.plastic && split)
+            throw synscale::SpecError("plastic group '" + g.name +
+                                      "': learning runs on one GPU (split worlds are not supported)");
     const ShardPlan plan = split ? plan_shards(net, R, cfg.shardMinSize, true) : ShardPlan{};
     const int smCount = device_props(cfg.device).smCount;
     auto init = [&](Impl& m, int rank, cudaStream_t shared) {
@@ -1893,6 +1952,21 @@ void DeviceEngine::spike_totals(std::vector<std::int64_t>& perPop) {
     if (nc) CK(cudaMemcpy(counts.data(), m.raster.countsAll, nc * 4, cudaMemcpyDeviceToHost));
     perPop.assign(np, 0);
     for (std::size_t i = 0; i < nc; ++i) perPop[i % np] += counts[i];
+}
+
+bool DeviceEngine::pull_weights(int group, float* dst, std::int64_t count) {
+    auto& m = *impl_;
+    for (const auto& L : m.stdp) {
+        if (L.gi != group) continue;
+        const auto& g = m.groupMeta[group];
+        if (count != static_cast<std::int64_t>(g.preCount) * g.nPost)
+            throw synscale::SpecError("wrong buffer size");
+        CK(cudaSetDevice(m.cfg.device));
+        CK(cudaStreamSynchronize(m.stream));
+        CK(cudaMemcpy(dst, L.dev[0].W, static_cast<std::size_t>(count) * 4, cudaMemcpyDeviceToHost));
+        return true;
+    }
+    return false;
 }
 
 void* DeviceEngine::stream() const { return impl_->stream; }

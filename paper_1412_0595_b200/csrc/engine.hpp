@@ -54,6 +54,9 @@ struct HostGroup {
     const std::int32_t* ind = nullptr;     // CRS postInd [nnz]
     const std::int64_t* rowStart = nullptr;  // CRS [nPre+1]
     std::int64_t nnz = 0;
+    // extension F2: STDP (fp32 constants; trace decays float(exp(-dt/tau)))
+    bool plastic = false;
+    float aPlus = 0, aMinus = 0, decPlus = 0, decMinus = 0, wMax = 0;
 };
 
 struct HostNet {
@@ -165,6 +168,8 @@ public:
     // in the background and returns -1.
     std::int64_t drain_raster(bool wait = true);
     void spike_totals(std::vector<std::int64_t>& perPop);
+    // A plastic group's current weights (false: the group is static).
+    bool pull_weights(int group, float* dst, std::int64_t count);
 
     // Neurons of population pop held by this process: [lo, lo + n) of
     // nGlobal.  State pull/push of a split population move that local slice

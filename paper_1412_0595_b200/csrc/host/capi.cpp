@@ -136,6 +136,14 @@ NetworkSpec to_spec(const ssb_net_desc* d) {
         s.storage = g.storage == SSB_STORAGE_DENSE ? StorageKind::Dense : StorageKind::Sparse;
         s.preOffset = g.pre_offset;
         s.preCount = g.pre_count;
+        s.stdp.enabled = g.plasticity == SSB_PLASTICITY_STDP;
+        s.stdp.aPlus = g.stdp_a_plus;
+        s.stdp.aMinus = g.stdp_a_minus;
+        s.stdp.tauPlusMs = g.stdp_tau_plus_ms;
+        s.stdp.tauMinusMs = g.stdp_tau_minus_ms;
+        s.stdp.wMax = g.stdp_w_max;
+        if (g.plasticity != SSB_PLASTICITY_NONE && g.plasticity != SSB_PLASTICITY_STDP)
+            throw SpecError("group '" + s.name + "': unknown plasticity kind");
         spec.synapses.push_back(std::move(s));
     }
     return spec;
@@ -215,6 +223,12 @@ ssb_net_desc* to_desc(const NetworkSpec& spec) {
         d.storage = g.storage == StorageKind::Dense ? SSB_STORAGE_DENSE : SSB_STORAGE_SPARSE;
         d.pre_offset = g.preOffset;
         d.pre_count = g.preCount;
+        d.plasticity = g.stdp.enabled ? SSB_PLASTICITY_STDP : SSB_PLASTICITY_NONE;
+        d.stdp_a_plus = g.stdp.aPlus;
+        d.stdp_a_minus = g.stdp.aMinus;
+        d.stdp_tau_plus_ms = g.stdp.tauPlusMs;
+        d.stdp_tau_minus_ms = g.stdp.tauMinusMs;
+        d.stdp_w_max = g.stdp.wMax;
         o->groupStore.push_back(d);
     }
     o->n_pops = static_cast<int32_t>(o->popStore.size());
@@ -805,6 +819,17 @@ int ssb_group_dense(const ssb_sim* sim, int32_t group, float* w, int64_t n) {
         if (!d) throw SpecError("group is stored sparse");
         if (n != static_cast<int64_t>(d->weights.size())) throw SpecError("wrong buffer size");
         std::memcpy(w, d->weights.data(), d->weights.size() * sizeof(float));
+    });
+}
+
+int ssb_group_weights(ssb_sim* sim, int32_t group, float* w, int64_t n) {
+    return on_sim(sim, [&](ssb::SimCore& c) {
+        if (group < 0 || group >= c.n_groups()) throw SpecError("group index out of range");
+        const auto* d = c.dense(group);
+        if (!d) throw SpecError("group is stored sparse");
+        if (n != static_cast<int64_t>(d->weights.size())) throw SpecError("wrong buffer size");
+        if (!c.engine().pull_weights(group, w, n))
+            std::memcpy(w, d->weights.data(), d->weights.size() * sizeof(float));
     });
 }
 

@@ -216,6 +216,15 @@ SimCore::SimCore(const NetworkSpec& spec, StorageMode mode, const EngineConfig& 
         g.nPost = spec_.populations[g.post].size;
         g.outDegree = gs.outDegree;
         g.dense = dense_[gi].has_value();
+        if (gs.stdp.enabled) {  // extension F2
+            if (!g.dense) throw SpecError("plastic group '" + gs.name + "' must be stored dense");
+            g.plastic = true;
+            g.aPlus = static_cast<float>(gs.stdp.aPlus);
+            g.aMinus = static_cast<float>(gs.stdp.aMinus);
+            g.decPlus = static_cast<float>(std::exp(-spec_.dtMs / gs.stdp.tauPlusMs));
+            g.decMinus = static_cast<float>(std::exp(-spec_.dtMs / gs.stdp.tauMinusMs));
+            g.wMax = static_cast<float>(gs.stdp.wMax);
+        }
         if (g.dense) {
             g.W = dense_[gi]->weights.data();
         } else {

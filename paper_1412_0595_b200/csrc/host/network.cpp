@@ -186,6 +186,21 @@ std::vector<Violation> validate(const NetworkSpec& spec) {
         if (auto msg = weight_problem(g.baseWeight); !msg.empty()) rep.add(at + ".baseWeight", msg);
         if (!fin(g.gScale) || g.gScale < 0.0)
             rep.add(at + ".gScale", "gScale must be finite and >= 0, got " + std::to_string(g.gScale));
+        if (g.stdp.enabled) {  // extension F2: dense all-to-all excitatory groups only
+            const auto& r = g.stdp;
+            if (g.storage != StorageKind::Dense)
+                rep.add(at + ".stdp", "a plastic group must be stored dense");
+            if (g.sign != SynapseSign::Excitatory)
+                rep.add(at + ".stdp", "a plastic group must be excitatory");
+            if (post != byName.end() && g.outDegree != post->second->size)
+                rep.add(at + ".stdp", "a plastic group must be all-to-all (outDegree = post size)");
+            if (!fin(r.aPlus) || r.aPlus < 0.0 || !fin(r.aMinus) || r.aMinus < 0.0)
+                rep.add(at + ".stdp", "aPlus and aMinus must be finite and >= 0");
+            if (!fin(r.tauPlusMs) || r.tauPlusMs <= 0.0 || !fin(r.tauMinusMs) || r.tauMinusMs <= 0.0)
+                rep.add(at + ".stdp", "trace time constants must be finite and > 0");
+            if (!fin(r.wMax) || r.wMax <= 0.0)
+                rep.add(at + ".stdp", "wMax must be finite and > 0");
+        }
     }
     return out;
 }

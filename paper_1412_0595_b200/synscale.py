@@ -141,6 +141,18 @@ class NeuronPopulation:
 
 
 @dataclass
+class StdpRule:
+    """Extension F2 (not in the reference): pair-based STDP on a
+    dense all-to-all excitatory group; the rule is include/synscale/synscale.hpp
+    StdpRule's (DESIGN.md §1 row A22)."""
+    aPlus: float = 0.0
+    aMinus: float = 0.0
+    tauPlusMs: float = 20.0
+    tauMinusMs: float = 20.0
+    wMax: float = 0.0
+
+
+@dataclass
 class SynapseGroupSpec:
     name: str
     pre: str
@@ -152,6 +164,7 @@ class SynapseGroupSpec:
     storage: StorageKind = StorageKind.Sparse
     preOffset: int = 0
     preCount: int = -1
+    stdp: Optional[StdpRule] = None  # extension F2
 
 
 @dataclass
@@ -268,6 +281,12 @@ class NetDesc:
             d.storage = int(g.storage)
             d.pre_offset = int(g.preOffset)
             d.pre_count = int(g.preCount)
+            if g.stdp is not None:
+                d.plasticity = L.PLASTICITY_STDP
+                d.stdp_a_plus, d.stdp_a_minus = float(g.stdp.aPlus), float(g.stdp.aMinus)
+                d.stdp_tau_plus_ms = float(g.stdp.tauPlusMs)
+                d.stdp_tau_minus_ms = float(g.stdp.tauMinusMs)
+                d.stdp_w_max = float(g.stdp.wMax)
         self._pops, self._groups = pops, groups
         self.desc = L.ssb_net_desc(len(spec.populations), pops, len(spec.synapses), groups,
                                    float(spec.dtMs), float(spec.durationMs),
@@ -304,7 +323,9 @@ def _spec_from_desc(d: L.ssb_net_desc) -> NetworkSpec:
                                                                   g.weight_value))
         spec.synapses.append(SynapseGroupSpec(
             g.name.decode(), g.pre.decode(), g.post.decode(), SynapseSign(g.sign), g.out_degree,
-            w, g.g_scale, StorageKind(g.storage), g.pre_offset, g.pre_count))
+            w, g.g_scale, StorageKind(g.storage), g.pre_offset, g.pre_count,
+            StdpRule(g.stdp_a_plus, g.stdp_a_minus, g.stdp_tau_plus_ms, g.stdp_tau_minus_ms,
+                     g.stdp_w_max) if g.plasticity == L.PLASTICITY_STDP else None))
     return spec
 
 
@@ -593,6 +614,17 @@ class Simulation:
             return None
         w = np.empty((npre.value, npost.value), np.float32)
         self._check(lib.ssb_group_dense(self._h, gi, _fptr(w), w.size))
+        return w
+
+    def group_weights(self, name: str) -> np.ndarray:
+        """A dense group's weights now: a plastic group's learned weights read
+        from the device (extension F2), a static group's group_dense()."""
+        gi = self.spec.group_index(name)
+        st, npre, npost, nnz = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
+        self._check(lib.ssb_group_info(self._h, gi, C.byref(st), C.byref(npre), C.byref(npost),
+                                       C.byref(nnz)))
+        w = np.empty((npre.value, npost.value), np.float32)
+        self._check(lib.ssb_group_weights(self._h, gi, _fptr(w), w.size))
         return w
 
     def group_sparse(self, name: str):

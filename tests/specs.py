@@ -171,3 +171,15 @@ def hh_mbody_spec(n_kc: int = 300, duration_ms: float = 30.0, seed: int = 7) -> 
                             kcModel=S.ModelKind.TraubMiles)
     return S.build_mbody_net(100, 20, n_kc, 100, {"pn_kc": 2.0, "pn_lhi": 1.0, "lhi_kc": 0.1,
                                                   "kc_dn": 30.0 / n_kc}, seed, o)
+
+
+def stdp_mbody_spec(n_kc: int, duration_ms: float, frac: float = 0.05, seed: int = 7,
+                    a_plus: float = 0.1, a_minus: float = 0.12, w_max: float = 3.0):
+    """Extension F2: the mushroom body with STDP on kc_dn (amplitudes and wMax
+    relative to the built kc_dn weight)."""
+    spec = mbody_spec(n_kc, frac, duration_ms, seed=seed)
+    g = spec.synapses[spec.group_index("kc_dn")]
+    w0 = g.baseWeight.value * g.gScale
+    g.stdp = S.StdpRule(aPlus=a_plus * w0, aMinus=a_minus * w0, tauPlusMs=20.0,
+                        tauMinusMs=15.0, wMax=w_max * w0)
+    return spec
