@@ -790,10 +790,13 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         }
     }
 
-    // windows per graph launch (overlap across windows needs an acyclic graph)
-    graphWindows = stepMode ? 1 : kMaxSets;
-    if (const char* e = std::getenv("SSB_GRAPH_WINDOWS"))
-        if (!stepMode) graphWindows = std::clamp(std::atoi(e), 1, kMaxSets);
+    // windows per graph launch.  Step mode (one-step windows) chains its
+    // steps inside a graph too: each step's updates wait on the previous
+    // step's deliveries (enqueue_windows), so a graph of many steps replaces a
+    // launch per step (SSB_STEP_GRAPH_WINDOWS=1 restores that).
+    graphWindows = kMaxSets;
+    if (const char* e = std::getenv(stepMode ? "SSB_STEP_GRAPH_WINDOWS" : "SSB_GRAPH_WINDOWS"))
+        graphWindows = std::clamp(std::atoi(e), 1, kMaxSets);
     {
         // The host runs at most kRing launches ahead of the last cursor it has
         // seen, so the arena must hold kRing + 1 launches of worst-case events
