@@ -464,6 +464,33 @@ def main():
                 "share_of_step": round(rf["share_of_step"], 4), "algorithmic": rf["unit"],
                 "kernels": rf["kernels"]}
 
+    # -- config 3 with KC->DN learning (extension F2, step mode): a bounded
+    # sample of 0.2 simulated seconds, device-timed, reported beside the
+    # static headline (BASELINE config 3 names learning)
+    learning = None
+    if world == 1 and not os.environ.get("SSB_BENCH_NO_LEARNING"):
+        import specs
+        lspec = specs.stdp_mbody_spec(N_KC, 1000.0)
+        lsim = S.Simulation(lspec, S.StorageMode.FromSpec, S.EngineOptions())
+        lsim.step(960)
+        lsim.sync()
+        c0 = lsim.spike_counts().copy()
+        l0 = lsim.kernel_launches()
+        st = torch.cuda.ExternalStream(lsim.stream())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        lsim.step(1920)
+        e1.record(st)
+        lsim.sync()
+        lms = e0.elapsed_time(e1)
+        lev = synaptic_events(lspec, lsim.spike_counts() - c0)
+        learning = {"workload": "config 3 + pair STDP on kc_dn (step mode), 1920 steps "
+                                "(0.192 s simulated, 40 graphs of 48 steps) after 960 warm-up steps",
+                    "value": lev / (lms / 1e3), "unit": UNIT, "sim_wall": 0.192 / (lms / 1e3),
+                    "us_per_timestep": lms * 1e3 / 1920,
+                    "gpu_launches": int(lsim.kernel_launches() - l0)}
+        lsim.close()
+
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
@@ -491,7 +518,7 @@ def main():
             "build_s": build_s,
             "step_ms": [round(x * 1e3, 3) for x in times],
             "gpu_launches": int(launches), "clocks": clk, "roofline": roofline,
-            "cpu_baseline": cpu, "e2e": e2e}
+            "cpu_baseline": cpu, "e2e": e2e, "learning": learning}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
