@@ -1041,6 +1041,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         D.x = alloc<float>(static_cast<std::size_t>(g.nPre));
         D.y = alloc<float>(static_cast<std::size_t>(g.nPost));
         D.preFlag = alloc<uint32_t>(static_cast<std::size_t>(nGroups));
+        D.ticket = alloc<unsigned>(1);
         D.nPre = g.nPre;
         D.nPost = g.nPost;
         D.preOffset = g.preOffset;
@@ -1349,8 +1350,6 @@ void DeviceEngine::Impl::enqueue_tail(int W, int b, cudaStream_t s) {
         launch("stdp_mark:" + nm, [&] { ssbk::stdp_mark_kernel<<<8, 256, 0, s>>>(D); });
         launch("stdp_update:" + nm,
                [&] { ssbk::stdp_update_kernel<<<L.grid, 256, L.smem, s>>>(D); });
-        launch("stdp_post_trace:" + nm,
-               [&] { ssbk::stdp_post_trace_kernel<<<1, 1024, 0, s>>>(D); });
     }
     launch("raster_window", [&] {
         ssbk::raster_window_kernel<<<W * raster.nPops, 256, 0, s>>>(rasterb[b], W);
