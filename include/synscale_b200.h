@@ -173,8 +173,9 @@ typedef struct ssb_engine_opts {
     /* split runs (world_size > 1, not virtual_world): 1 = each rank records
      * only its own neurons of split populations, and rank 0 alone the whole
      * (replicated) ones; the global raster is the union over ranks (spike
-     * counts likewise sum over ranks).  0 = every rank records the global
-     * raster. */
+     * counts likewise sum over ranks; ssb_finish's rates are already the
+     * global ones: it all-reduces the per-population totals).  0 = every
+     * rank records the global raster. */
     int32_t raster_local;
 } ssb_engine_opts;
 

@@ -240,3 +240,135 @@ def ref_time_steps(desc_ptr, mode: int, steps: int, replicas: int):
     t = ref_lib().ref_time_steps(C.cast(desc_ptr, C.c_void_p), mode, steps, replicas,
                                  C.byref(build_s), C.byref(ev))
     return t, build_s.value
+
+
+# ---- the reference's own builders and replica pools (ref_shim.cpp) ------------------
+
+def mbody_gscales(n_kc: int, frac: float):
+    """SURVEY.md §8(d) gScales: pn_kc, pn_lhi, lhi_kc, kc_dn."""
+    return (0.5 / frac, 1.0, 0.1, 30.0 / n_kc)
+
+
+def _bind_builders(lib: C.CDLL) -> None:
+    if getattr(lib, "_builders_bound", False):
+        return
+    d4 = _P(_dbl)
+    lib.ref_build_mbody.restype = _vp
+    lib.ref_build_mbody.argtypes = [_i32, _i32, _i32, _i32, d4, _u64, _dbl, _dbl, _dbl, _dbl,
+                                    C.c_char_p, C.c_size_t]
+    lib.ref_build_izhikevich.restype = _vp
+    lib.ref_build_izhikevich.argtypes = [_i32, _i32, _dbl, _dbl, _u64, _dbl, _dbl, _dbl, _dbl,
+                                         _dbl, _dbl, _dbl, C.c_int, C.c_char_p, C.c_size_t]
+    lib.ref_desc_free.restype, lib.ref_desc_free.argtypes = None, [_vp]
+    lib.ref_pool_mbody.restype = _vp
+    lib.ref_pool_mbody.argtypes = [_i32, _i32, _i32, _i32, d4, _u64, _dbl, _dbl, _dbl, _dbl,
+                                   C.c_int, C.c_int, _P(_dbl), C.c_char_p, C.c_size_t]
+    lib.ref_pool_step.restype, lib.ref_pool_step.argtypes = _dbl, [_vp, C.c_longlong]
+    lib.ref_pool_counts.restype = C.c_int
+    lib.ref_pool_counts.argtypes = [_vp, C.c_longlong, C.c_longlong, _vp, C.c_int]
+    lib.ref_pool_groups.restype = C.c_int
+    lib.ref_pool_groups.argtypes = [_vp, _vp, _vp, C.c_int]
+    lib.ref_pool_steps_total.restype, lib.ref_pool_steps_total.argtypes = C.c_longlong, [_vp]
+    lib.ref_pool_destroy.restype, lib.ref_pool_destroy.argtypes = None, [_vp]
+    lib.ref_pool_raster_checksum.restype = _u64
+    lib.ref_pool_raster_checksum.argtypes = [_vp, C.c_int, C.c_longlong]
+    lib._builders_bound = True
+
+
+class RefDesc:
+    """A flat ssb_net_desc built by the REFERENCE's own builder (build_mbody_net /
+    build_izhikevich_net, network.cpp:198-362), owned by the shim."""
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+        self._lib = ref_lib()
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            self._lib.ref_desc_free(self.ptr)
+            self.ptr = None
+
+
+def ref_mbody_desc(n_kc: int, frac: float, duration_ms: float, seed: int = 7,
+                   dt_ms: float = 0.1, n_pn: int = 100, n_lhi: int = 20, n_dn: int = 100,
+                   rate_hz: float = 50.0, gscales=None) -> RefDesc:
+    lib = ref_lib()
+    _bind_builders(lib)
+    g = (_dbl * 4)(*(gscales or mbody_gscales(n_kc, frac)))
+    err = C.create_string_buffer(1024)
+    p = lib.ref_build_mbody(n_pn, n_lhi, n_kc, n_dn, g, seed, dt_ms, duration_ms, rate_hz, frac,
+                            err, len(err))
+    if not p:
+        raise ValueError(err.value.decode())
+    return RefDesc(p)
+
+
+def ref_izh_desc(n: int, n_conn: int, exc_fraction: float, g_scale: float, seed: int,
+                 dt_ms: float = 1.0, duration_ms: float = 1000.0, noise_exc: float = 5.0,
+                 noise_inh: float = 2.0, exc_hi: float = 0.5, inh_hi: float = 1.0,
+                 bias: float = 0.0, dense: bool = False) -> RefDesc:
+    lib = ref_lib()
+    _bind_builders(lib)
+    err = C.create_string_buffer(1024)
+    p = lib.ref_build_izhikevich(n, n_conn, exc_fraction, g_scale, seed, dt_ms, duration_ms,
+                                 noise_exc, noise_inh, exc_hi, inh_hi, bias, int(dense), err,
+                                 len(err))
+    if not p:
+        raise ValueError(err.value.decode())
+    return RefDesc(p)
+
+
+class RefPool:
+    """`replicas` reference Simulations of the reference-built mushroom body,
+    stepped concurrently on host threads (calibration.cpp:76-84's model)."""
+
+    def __init__(self, n_kc: int, frac: float, duration_ms: float, replicas: int, seed: int = 7,
+                 mode: int = 0, dt_ms: float = 0.1):
+        self.lib = ref_lib()
+        _bind_builders(self.lib)
+        g = (_dbl * 4)(*mbody_gscales(n_kc, frac))
+        err = C.create_string_buffer(1024)
+        b = C.c_double()
+        self.h = self.lib.ref_pool_mbody(100, 20, n_kc, 100, g, seed, dt_ms, duration_ms, 50.0,
+                                         frac, mode, replicas, C.byref(b), err, len(err))
+        if not self.h:
+            raise ValueError(err.value.decode())
+        self.build_s = b.value
+        self.replicas = replicas
+        pre = np.zeros(16, np.int32)
+        deg = np.zeros(16, np.int32)
+        n = self.lib.ref_pool_groups(self.h, pre.ctypes.data, deg.ctypes.data, 16)
+        self.group_pre, self.group_out = pre[:n], deg[:n]
+
+    def step(self, steps: int) -> float:
+        t = self.lib.ref_pool_step(self.h, steps)
+        if t < 0:
+            raise RuntimeError("reference step failed")
+        return t
+
+    def counts(self, lo: int, hi: int) -> np.ndarray:
+        """Spikes per population with step in [lo, hi), summed over replicas
+        (finishes the replicas on first use)."""
+        out = np.zeros(16, np.int64)
+        n = self.lib.ref_pool_counts(self.h, lo, hi, out.ctypes.data, 16)
+        if n < 0:
+            raise RuntimeError("reference finish failed")
+        return out[:n]
+
+    def synaptic_events(self, lo: int, hi: int) -> int:
+        c = self.counts(lo, hi)
+        return int(sum(int(c[p]) * int(d) for p, d in zip(self.group_pre, self.group_out)))
+
+    def raster_checksum(self, replica: int = 0, up_to: int = 1 << 62) -> int:
+        self.counts(0, 0)
+        return int(self.lib.ref_pool_raster_checksum(self.h, replica, up_to))
+
+    def steps_total(self) -> int:
+        return int(self.lib.ref_pool_steps_total(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ref_pool_destroy(self.h)
+            self.h = None
+
+    __del__ = close

@@ -360,3 +360,269 @@ REF_API double ref_time_steps(const ssb_net_desc* d, int mode, long long steps, 
         return -1.0;
     }
 }
+
+// ---------------------------------------------------------------------------
+// The reference's OWN builders (network.cpp:198-362), flattened here, so the
+// golden fixtures, the builder-equality test and the bench reference arm never
+// take a spec from the product library.
+namespace {
+
+struct OwnedDesc {
+    ssb_net_desc d{};  // first member: an OwnedDesc* is an ssb_net_desc*
+    std::vector<ssb_pop_desc> pops;
+    std::vector<ssb_group_desc> groups;
+    std::vector<std::unique_ptr<std::string>> strs;
+    std::vector<std::unique_ptr<std::vector<double>>> arrs;
+
+    const char* keep(const std::string& s) {
+        strs.push_back(std::make_unique<std::string>(s));
+        return strs.back()->c_str();
+    }
+    const double* keep(const std::vector<double>& v) {
+        arrs.push_back(std::make_unique<std::vector<double>>(v));
+        return arrs.back()->data();
+    }
+};
+
+OwnedDesc* flatten(const NetworkSpec& s) {
+    auto o = std::make_unique<OwnedDesc>();
+    for (const auto& p : s.populations) {
+        ssb_pop_desc q{};
+        q.name = o->keep(p.name);
+        q.size = p.size;
+        q.seed = p.seed;
+        if (p.model == ModelKind::PoissonSource) {
+            q.model = SSB_MODEL_POISSON;
+            q.rate_hz = std::get<PoissonParams>(p.params).rateHz;
+        } else if (p.model == ModelKind::CondLif) {
+            q.model = SSB_MODEL_CONDLIF;
+            const auto& c = std::get<CondLifParams>(p.params);
+            q.tau_m_ms = c.tauMMs;
+            q.e_leak_mv = c.eLeakMV;
+            q.v_thresh_mv = c.vThreshMV;
+            q.v_reset_mv = c.vResetMV;
+            q.e_exc_mv = c.eExcMV;
+            q.e_inh_mv = c.eInhMV;
+            q.tau_syn_ms = c.tauSynMs;
+        } else {
+            q.model = SSB_MODEL_IZHIKEVICH;
+            const auto& z = std::get<IzhikevichParams>(p.params);
+            q.izh_a = o->keep(z.a);
+            q.izh_b = o->keep(z.b);
+            q.izh_c = o->keep(z.c);
+            q.izh_d = o->keep(z.d);
+            q.izh_noise = o->keep(z.noiseAmplitude);
+            q.izh_bias = o->keep(z.biasCurrent);
+        }
+        o->pops.push_back(q);
+    }
+    for (const auto& g : s.synapses) {
+        ssb_group_desc q{};
+        q.name = o->keep(g.name);
+        q.pre = o->keep(g.pre);
+        q.post = o->keep(g.post);
+        q.sign = g.sign == SynapseSign::Inhibitory ? SSB_SIGN_INH : SSB_SIGN_EXC;
+        q.out_degree = g.outDegree;
+        if (g.baseWeight.kind == WeightDist::Kind::Uniform) {
+            q.weight_kind = SSB_WEIGHT_UNIFORM;
+            q.weight_lo = g.baseWeight.lo;
+            q.weight_hi = g.baseWeight.hi;
+        } else {
+            q.weight_kind = SSB_WEIGHT_CONSTANT;
+            q.weight_value = g.baseWeight.value;
+        }
+        q.g_scale = g.gScale;
+        q.storage = g.storage == StorageKind::Dense ? SSB_STORAGE_DENSE : SSB_STORAGE_SPARSE;
+        q.pre_offset = g.preOffset;
+        q.pre_count = g.preCount;
+        o->groups.push_back(q);
+    }
+    o->d.n_pops = static_cast<int32_t>(o->pops.size());
+    o->d.pops = o->pops.data();
+    o->d.n_groups = static_cast<int32_t>(o->groups.size());
+    o->d.groups = o->groups.data();
+    o->d.dt_ms = s.dtMs;
+    o->d.duration_ms = s.durationMs;
+    o->d.global_seed = s.globalSeed;
+    return o.release();
+}
+
+NetworkSpec mbody(int32_t nPN, int32_t nLHI, int32_t nKC, int32_t nDN, const double g[4],
+                  uint64_t seed, double dtMs, double durationMs, double pnRateHz, double frac) {
+    MBodyBuildOptions o;
+    o.dtMs = dtMs;
+    o.durationMs = durationMs;
+    o.pnRateHz = pnRateHz;
+    o.pnKcOutFraction = frac;
+    return build_mbody_net(nPN, nLHI, nKC, nDN,
+                           {{"pn_kc", g[0]}, {"pn_lhi", g[1]}, {"lhi_kc", g[2]}, {"kc_dn", g[3]}},
+                           seed, o);
+}
+
+// Replicas of one reference Simulation stepped concurrently on host threads
+// (the calibration sweep's parallelism model, calibration.cpp:76-84).
+struct RefPool {
+    NetworkSpec spec;
+    std::vector<std::unique_ptr<Simulation>> sims;
+    std::vector<RunResult> results;
+};
+
+template <class F>
+void on_threads(int n, F&& f) {
+    std::vector<std::thread> th;
+    for (int i = 0; i < n; ++i) th.emplace_back([&, i] { f(i); });
+    for (auto& t : th) t.join();
+}
+
+}  // namespace
+
+// build_mbody_net of the reference (network.cpp:286-362), flattened.  gscales
+// order: pn_kc, pn_lhi, lhi_kc, kc_dn.  Release with ref_desc_free.
+REF_API ssb_net_desc* ref_build_mbody(int32_t nPN, int32_t nLHI, int32_t nKC, int32_t nDN,
+                                      const double* gscales, uint64_t seed, double dtMs,
+                                      double durationMs, double pnRateHz, double frac, char* err,
+                                      std::size_t errlen) {
+    try {
+        return &flatten(mbody(nPN, nLHI, nKC, nDN, gscales, seed, dtMs, durationMs, pnRateHz,
+                              frac))->d;
+    } catch (const std::exception& e) {
+        fail(e, err, errlen);
+        return nullptr;
+    }
+}
+
+// build_izhikevich_net of the reference (network.cpp:198-284), flattened.
+REF_API ssb_net_desc* ref_build_izhikevich(int32_t n, int32_t nConn, double excFraction,
+                                           double gScale, uint64_t seed, double dtMs,
+                                           double durationMs, double noiseExc, double noiseInh,
+                                           double excWeightHi, double inhWeightHi, double bias,
+                                           int dense, char* err, std::size_t errlen) {
+    try {
+        IzhBuildOptions o;
+        o.dtMs = dtMs;
+        o.durationMs = durationMs;
+        o.noiseExc = noiseExc;
+        o.noiseInh = noiseInh;
+        o.excWeightHi = excWeightHi;
+        o.inhWeightHi = inhWeightHi;
+        o.biasCurrent = bias;
+        o.storage = dense ? StorageKind::Dense : StorageKind::Sparse;
+        return &flatten(build_izhikevich_net(n, nConn, excFraction, gScale, seed, o))->d;
+    } catch (const std::exception& e) {
+        fail(e, err, errlen);
+        return nullptr;
+    }
+}
+
+REF_API void ref_desc_free(ssb_net_desc* d) { delete reinterpret_cast<OwnedDesc*>(d); }
+
+// `replicas` Simulations of the reference's own mushroom body, constructed
+// concurrently; *buildSeconds = construction wall time.
+REF_API RefPool* ref_pool_mbody(int32_t nPN, int32_t nLHI, int32_t nKC, int32_t nDN,
+                                const double* gscales, uint64_t seed, double dtMs,
+                                double durationMs, double pnRateHz, double frac, int mode,
+                                int replicas, double* buildSeconds, char* err,
+                                std::size_t errlen) {
+    try {
+        auto p = std::make_unique<RefPool>();
+        p->spec = mbody(nPN, nLHI, nKC, nDN, gscales, seed, dtMs, durationMs, pnRateHz, frac);
+        p->sims.resize(static_cast<std::size_t>(replicas));
+        const auto b0 = std::chrono::steady_clock::now();
+        std::vector<std::string> errs(static_cast<std::size_t>(replicas));
+        on_threads(replicas, [&](int i) {
+            try {
+                p->sims[i] = std::make_unique<Simulation>(p->spec, to_mode(mode));
+            } catch (const std::exception& e) {
+                errs[i] = e.what();
+            }
+        });
+        for (const auto& e : errs)
+            if (!e.empty()) throw SpecError(e);
+        if (buildSeconds)
+            *buildSeconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - b0)
+                                .count();
+        return p.release();
+    } catch (const std::exception& e) {
+        fail(e, err, errlen);
+        return nullptr;
+    }
+}
+
+// Advances every replica by `steps` Simulation::step() calls, one host thread
+// per replica; returns the wall seconds of the whole pool (-1 on error).
+REF_API double ref_pool_step(RefPool* p, long long steps) {
+    std::vector<int> bad(p->sims.size(), 0);
+    const auto t0 = std::chrono::steady_clock::now();
+    on_threads(static_cast<int>(p->sims.size()), [&](int i) {
+        try {
+            for (long long s = 0; s < steps; ++s) p->sims[i]->step();
+        } catch (const std::exception&) {
+            bad[i] = 1;
+        }
+    });
+    const double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (int b : bad)
+        if (b) return -1.0;
+    return t;
+}
+
+// Finishes every replica (Simulation::finish, outside any timed region) and
+// writes, per population, the spikes with step in [lo, hi) summed over the
+// replicas.  Returns the population count, or -1.
+REF_API int ref_pool_counts(RefPool* p, long long lo, long long hi, long long* counts, int cap) {
+    try {
+        const int nPops = static_cast<int>(p->spec.populations.size());
+        if (cap < nPops) return -1;
+        if (p->results.empty()) {
+            p->results.resize(p->sims.size());
+            on_threads(static_cast<int>(p->sims.size()),
+                       [&](int i) { p->results[i] = p->sims[i]->finish(); });
+        }
+        for (int k = 0; k < nPops; ++k) counts[k] = 0;
+        for (const auto& r : p->results)
+            for (const auto& ev : r.raster.events)
+                if (ev.step >= lo && ev.step < hi) ++counts[ev.population];
+        return nPops;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// Per group: index of its pre population and its outDegree (synaptic events =
+// pre spikes x outDegree).  Returns the group count.
+REF_API int ref_pool_groups(RefPool* p, int32_t* prePop, int32_t* outDegree, int cap) {
+    const auto& s = p->spec;
+    const int n = static_cast<int>(s.synapses.size());
+    for (int g = 0; g < n && g < cap; ++g) {
+        int idx = 0;
+        for (std::size_t k = 0; k < s.populations.size(); ++k)
+            if (s.populations[k].name == s.synapses[g].pre) idx = static_cast<int>(k);
+        prePop[g] = idx;
+        outDegree[g] = s.synapses[g].outDegree;
+    }
+    return n;
+}
+
+REF_API long long ref_pool_steps_total(RefPool* p) { return p->sims.at(0)->steps_total(); }
+REF_API void ref_pool_destroy(RefPool* p) { delete p; }
+
+// Raster of a single reference run as the order-independent checksum used by
+// the split parity check (tests/specs.py raster_checksum): sum over events of
+// mix64(step << 40 ^ pop << 32 ^ neuron), mod 2^64, events with step < upTo.
+REF_API uint64_t ref_pool_raster_checksum(RefPool* p, int replica, long long upTo) {
+    const auto& r = p->results.at(static_cast<std::size_t>(replica));
+    uint64_t acc = 0;
+    for (const auto& ev : r.raster.events) {
+        if (ev.step >= upTo) continue;
+        uint64_t x = (static_cast<uint64_t>(ev.step) << 40) ^
+                     (static_cast<uint64_t>(ev.population) << 32) ^
+                     static_cast<uint64_t>(static_cast<uint32_t>(ev.neuron));
+        x ^= x >> 30;
+        x *= 0xbf58476d1ce4e5b9ULL;
+        x ^= x >> 27;
+        x *= 0x94d049bb133111ebULL;
+        x ^= x >> 31;
+        acc += x;
+    }
+    return acc;
+}

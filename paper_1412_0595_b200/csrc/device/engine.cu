@@ -34,6 +34,18 @@ void check(cudaError_t e, const char* what) {
 
 int round_up(int v, int u) { return (v + u - 1) / u * u; }
 
+// Raises (never lowers) a kernel's dynamic shared-memory limit.  The limit is
+// per function and process-wide, so engines built concurrently (sweep
+// workers) and groups with different needs go through one lock.
+std::mutex gSmemLimitMutex;
+void allow_smem(const void* fn, int bytes) {
+    std::lock_guard<std::mutex> lk(gSmemLimitMutex);
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, fn));
+    if (fa.maxDynamicSharedSizeBytes < bytes)
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
 // Host store of drained raster events: anonymous mappings with transparent
 // huge pages (first touch of tens of MB in 4 KB pages costs more than the
 // device-to-host copy itself).
@@ -1032,8 +1044,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         if (L.smem > 200 * 1024)
             throw synscale::SpecError("plastic group '" + g.name + "': too many post neurons");
         if (L.smem > 48 * 1024)
-            CK(cudaFuncSetAttribute(ssbk::stdp_update_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem));
+            allow_smem(reinterpret_cast<const void*>(&ssbk::stdp_update_kernel), L.smem);
         const int nGroups = (g.nPre + 31) / 32;
         L.grid = std::max(1, std::min((nGroups + 7) / 8, 8 * smCount));
         ssbk::StdpDev D{};
@@ -1132,12 +1143,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     // process-wide: only ever raised, several engines may share a device)
     int maxSmem = 0;
     for (const auto& P : pops) maxSmem = std::max(maxSmem, P.smemBytes);
-    auto allow = [](const void* fn, int bytes) {
-        cudaFuncAttributes fa;
-        CK(cudaFuncGetAttributes(&fa, fn));
-        if (fa.maxDynamicSharedSizeBytes < bytes)
-            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    };
+    auto allow = allow_smem;
     allow(reinterpret_cast<const void*>(&ssbk::condlif_window_kernel), std::max(maxSmem, 4096));
     allow(reinterpret_cast<const void*>(&ssbk::izh_window_kernel), std::max(maxSmem, 4096));
     allow(reinterpret_cast<const void*>(&ssbk::hh_window_kernel), std::max(maxSmem, 4096));
@@ -1955,6 +1961,20 @@ void DeviceEngine::spike_totals(std::vector<std::int64_t>& perPop) {
     perPop.assign(np, 0);
     for (std::size_t i = 0; i < nc; ++i) perPop[i % np] += counts[i];
 }
+
+void DeviceEngine::global_spike_totals(std::vector<std::int64_t>& perPop) {
+    spike_totals(perPop);
+    auto& m = *impl_;
+    if (!m.rasterLocal || !m.comm || perPop.empty()) return;
+    const std::size_t bytes = perPop.size() * 8;
+    auto* tmp = reinterpret_cast<unsigned long long*>(m.comm_scratch(bytes));
+    CK(cudaMemcpyAsync(tmp, perPop.data(), bytes, cudaMemcpyHostToDevice, m.stream));
+    m.comm->allreduce_sum_u64(tmp, perPop.size(), m.stream);
+    CK(cudaMemcpyAsync(perPop.data(), tmp, bytes, cudaMemcpyDeviceToHost, m.stream));
+    CK(cudaStreamSynchronize(m.stream));
+}
+
+bool DeviceEngine::raster_discarded() const { return impl_->rasterDiscarded; }
 
 bool DeviceEngine::pull_weights(int group, float* dst, std::int64_t count) {
     auto& m = *impl_;

@@ -168,6 +168,10 @@ public:
     // in the background and returns -1.
     std::int64_t drain_raster(bool wait = true);
     void spike_totals(std::vector<std::int64_t>& perPop);
+    // spike_totals summed over the ranks of a split run that records local
+    // rasters (one all-reduce); otherwise spike_totals.
+    void global_spike_totals(std::vector<std::int64_t>& perPop);
+    bool raster_discarded() const;
     // A plastic group's current weights (false: the group is static).
     bool pull_weights(int group, float* dst, std::int64_t count);
 

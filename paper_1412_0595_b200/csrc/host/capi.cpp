@@ -863,6 +863,7 @@ int ssb_result_rates(const ssb_sim* sim, double* rates, int32_t n_pops) {
     return on_sim(const_cast<ssb_sim*>(sim), [&](ssb::SimCore& c) {
         if (!c.finished()) throw SpecError("results are available after finish");
         if (n_pops != c.n_pops()) throw SpecError("wrong population count");
+        if (static_cast<int>(c.rates().size()) != n_pops) throw SpecError("no rates recorded");
         for (int i = 0; i < n_pops; ++i) rates[i] = c.rates()[i];
     });
 }

@@ -265,20 +265,28 @@ void SimCore::finish() {
     if (finished_) throw SpecError("finish() may only be called once");
     if (done_ < net_.steps) step(net_.steps - done_);
     engine_->sync();
-    finished_ = true;
-    engine_->collect_raster(counts_, neurons_);
+    // the raster (unless discarded by ssb_raster_discard) and the rates: the
+    // rates come from the device's per-step counts, summed over the ranks of a
+    // split run that records local rasters, so they never depend on the raster
+    std::vector<std::int32_t> counts, neurons;
+    if (!engine_->raster_discarded()) engine_->collect_raster(counts, neurons);
+    std::vector<std::int64_t> perPop;
+    engine_->global_spike_totals(perPop);
     const std::size_t np = spec_.populations.size();
-    std::vector<std::int64_t> perPop(np, 0);
-    for (std::size_t i = 0; i < counts_.size(); ++i) perPop[i % np] += counts_[i];
-    rates_.resize(np);
-    sumNaNs_ = 0;
+    std::vector<double> rates(np);
+    std::int64_t nans = 0;
     for (std::size_t p = 0; p < np; ++p) {
-        rates_[p] = spike_rate(perPop[p], spec_.populations[p].size, spec_.durationMs);
+        rates[p] = spike_rate(perPop.at(p), spec_.populations[p].size, spec_.durationMs);
         std::int64_t f = 0;
         engine_->pull(static_cast<int>(p), kFieldFlagged, &f, 1);
-        sumNaNs_ += f;
+        nans += f;
     }
+    counts_ = std::move(counts);
+    neurons_ = std::move(neurons);
+    rates_ = std::move(rates);
+    sumNaNs_ = nans;
     wallMs_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
+    finished_ = true;
 }
 
 RunResult SimCore::run_result() const {

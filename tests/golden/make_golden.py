@@ -39,8 +39,10 @@ GENS = [  # nPre, nPost, k, kind, lo, hi, value, sign, seed
 ]
 
 
-def run_ref(spec, mode):
-    d = S.NetDesc(spec)
+def run_ref(spec, mode, desc=None, light=False):
+    """One reference run.  `desc`: a flat spec the reference's own builder made
+    (the mushroom-body and Izhikevich runs); otherwise `spec` flattened."""
+    d = desc if desc is not None else S.NetDesc(spec)
     sim = O.CpuSim(d.ptr, spec, int(mode), ref=True)
     step, pop, neu = sim.finish()
     out = {
@@ -52,13 +54,16 @@ def run_ref(spec, mode):
         "state_sha": {},
         "groups": {},
         "head": [[int(a), int(b), int(c)] for a, b, c in zip(step[:40], pop[:40], neu[:40])],
+        "checksum": str(specs.raster_checksum(step, pop, neu)),
     }
+    if light:
+        del out["groups"]
     for pi, p in enumerate(spec.populations):
         fields = ("v", "gExc", "gInh", "excIn", "inhIn", "nanFlag")
         if p.model == S.ModelKind.Izhikevich:
             fields = ("v", "u", "excIn", "inhIn", "nanFlag")
         out["state_sha"][p.name] = {f: specs.sha(sim.state(pi, f)) for f in fields}
-    for gi, g in enumerate(spec.synapses):
+    for gi, g in enumerate(spec.synapses if not light else []):
         kind, m = sim.group(gi)
         out["groups"][g.name] = [kind, specs.sha(*(m if kind == "sparse" else (m,)))]
     return out
@@ -82,22 +87,54 @@ def main():
         gens.append(entry)
     gold["gen_fixed_outdegree"] = gens
 
+    def mbody(cfg, ms):
+        """(desc, spec) of BASELINE config `cfg` from the reference's build_mbody_net."""
+        n_kc, frac, _ = specs.CONFIGS[cfg]
+        return specs.ref_mbody_spec(n_kc, frac, ms)
+
+    def izh(duration_ms=1000.0, dense=False):
+        d = O.ref_izh_desc(1000, 100, 0.8, 6.0, 1, duration_ms=duration_ms, dense=dense)
+        return d, specs.spec_from_ref_desc(d)
+
+    M = S.StorageMode
     runs = {}
-    for name, (spec, mode) in {
-        "cfg1_1000ms": specs.config_spec(1, 1000.0),
-        "cfg2_100ms": specs.config_spec(2, 100.0),
-        "cfg3_20ms": specs.config_spec(3, 20.0),
-        "cfg1_sparse_300ms": (specs.config_spec(1, 300.0)[0], S.StorageMode.ForceSparse),
-        "cfg2_fromspec_100ms": (specs.config_spec(2, 100.0)[0], S.StorageMode.FromSpec),
-        "chain_100ms": (specs.chain_spec(100.0), S.StorageMode.FromSpec),
-        "recurrent_200ms": (specs.recurrent_lif_spec(), S.StorageMode.FromSpec),
-        "izh_1000_1000ms": (specs.izh_spec(), S.StorageMode.FromSpec),
-        "izh_1000_dense_300ms": (specs.izh_spec(duration_ms=300.0), S.StorageMode.ForceDense),
-        "izh_ff_200ms": (specs.izh_ff_spec(), S.StorageMode.FromSpec),
+    for name, (built, mode, light) in {
+        "cfg1_1000ms": (mbody(1, 1000.0), M.ForceDense, False),
+        "cfg2_100ms": (mbody(2, 100.0), M.ForceSparse, False),
+        "cfg3_20ms": (mbody(3, 20.0), M.FromSpec, False),
+        "cfg1_sparse_300ms": (mbody(1, 300.0), M.ForceSparse, False),
+        "cfg2_fromspec_100ms": (mbody(2, 100.0), M.FromSpec, False),
+        "chain_100ms": ((None, specs.chain_spec(100.0)), M.FromSpec, False),
+        "recurrent_200ms": ((None, specs.recurrent_lif_spec()), M.FromSpec, False),
+        "izh_1000_1000ms": (izh(), M.FromSpec, False),
+        "izh_1000_dense_300ms": (izh(300.0), M.ForceDense, False),
+        "izh_ff_200ms": ((None, specs.izh_ff_spec()), M.FromSpec, False),
+        # BASELINE config 3 over its whole 1 s (10,000 steps) and config 4
+        # (1M KC) over 100 ms (1,000 steps, four 256-step windows)
+        "cfg3_1000ms": (mbody(3, 1000.0), M.FromSpec, True),
+        "cfg4_100ms": (mbody(4, 100.0), M.FromSpec, True),
     }.items():
         print("reference run", name, flush=True)
-        runs[name] = run_ref(spec, mode)
+        desc, spec = built
+        runs[name] = run_ref(spec, mode, desc, light)
     gold["runs"] = runs
+
+    # bench.py's end-of-run parity check: the split network of N x 100k KC
+    # (and config 4) over 100 ms, as spike counts + order-independent raster
+    # checksum (bench.raster_checksum); the reference's own builder and engine
+    bp = {"source": gold["source"], "duration_ms": 100.0,
+          "checksum": "sum of mix64(step<<40 ^ pop<<32 ^ neuron) mod 2^64 (bench.raster_checksum)",
+          "runs": {}}
+    for key, n_kc in (("split1", 100_000), ("split2", 200_000), ("split4", 400_000),
+                      ("split8", 800_000), ("cfg4", 1_000_000)):
+        print("reference parity run", key, flush=True)
+        pool = O.RefPool(n_kc, 0.05, 100.0, 1)
+        pool.step(pool.steps_total())
+        bp["runs"][key] = {"n_kc": n_kc, "counts": [int(c) for c in pool.counts(0, 1 << 62)],
+                           "checksum": str(pool.raster_checksum())}
+        pool.close()
+    with open(os.path.join(OUT, "bench_parity.json"), "w") as f:
+        json.dump(bp, f, indent=1, sort_keys=True)
 
     # CondLif + Poisson known-answer network (test_engine.cpp:183-290): the
     # reference's per-step v / gExc / gInh of the single conductance neuron.

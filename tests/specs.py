@@ -183,3 +183,43 @@ def stdp_mbody_spec(n_kc: int, duration_ms: float, frac: float = 0.05, seed: int
     g.stdp = S.StdpRule(aPlus=a_plus * w0, aMinus=a_minus * w0, tauPlusMs=20.0,
                         tauMinusMs=15.0, wMax=w_max * w0)
     return spec
+
+
+def spec_from_ref_desc(desc) -> S.NetworkSpec:
+    """The product-side NetworkSpec view of a flat ssb_net_desc that the
+    REFERENCE's own builder produced (oracle.RefDesc); a pure data conversion."""
+    import ctypes as C
+    from paper_1412_0595_b200 import _lib as L
+    return S._spec_from_desc(C.cast(desc.ptr, C.POINTER(L.ssb_net_desc)).contents)
+
+
+def spec_key(spec: S.NetworkSpec):
+    """Every field of a spec as a comparable tuple (float arrays by their bytes)."""
+    def val(x):
+        if isinstance(x, (list, tuple, np.ndarray)):
+            return np.ascontiguousarray(x, np.float64).tobytes()
+        return x
+
+    def fields(obj):
+        if obj is None:
+            return None
+        return tuple((k, val(v) if not hasattr(v, "__dataclass_fields__") else fields(v))
+                     for k, v in sorted(vars(obj).items()))
+    return (spec.dtMs, spec.durationMs, spec.globalSeed,
+            tuple(fields(p) for p in spec.populations), tuple(fields(g) for g in spec.synapses))
+
+
+def ref_mbody_spec(n_kc: int, frac: float, duration_ms: float, seed: int = 7):
+    """(RefDesc, spec view) of the mushroom body built by the reference's
+    build_mbody_net (network.cpp:286-362) with the §8(d) gScales."""
+    from oracle import oracle as O
+    d = O.ref_mbody_desc(n_kc, frac, duration_ms, seed=seed)
+    return d, spec_from_ref_desc(d)
+
+
+def raster_checksum(step, pop, neuron) -> int:
+    """Order-independent raster checksum (sum of mix64(step<<40 ^ pop<<32 ^ neuron)
+    mod 2^64); the same function as bench.raster_checksum and the shim's
+    ref_pool_raster_checksum."""
+    import bench
+    return bench.raster_checksum(step, pop, neuron)

@@ -565,3 +565,61 @@ def test_traubmiles_kcs_match_restatement(oracle_mod, kw):
     rg, ro = g.finish(), o.finish()
     assert np.array_equal(rg.raster.neuron, ro[2]) and np.array_equal(rg.raster.step, ro[0])
     assert np.count_nonzero(rg.raster.population == kc) > 100
+
+
+# ---- BASELINE configs 3 and 4 at their bench horizons ------------------------
+
+def assert_matches_golden_run(sim, r, spec, g):
+    counts = [int(np.count_nonzero(r.raster.population == i)) for i in range(len(spec.populations))]
+    assert counts == g["counts"]
+    assert len(r.raster) == g["n_events"]
+    assert specs.sha(r.raster.step, r.raster.population, r.raster.neuron) == g["raster_sha"]
+    assert specs.raster_checksum(r.raster.step, r.raster.population, r.raster.neuron) == \
+        int(g["checksum"])
+    assert [r.avgSpike[p.name] for p in spec.populations] == g["rates"]
+    assert r.sumNaNs == g["sum_nans"]
+    for pi, p in enumerate(spec.populations):
+        for f, h in g["state_sha"][p.name].items():
+            if p.model == S.ModelKind.PoissonSource and f in ("v", "gExc", "gInh"):
+                continue
+            assert specs.sha(sim.pull(pi, f)) == h, (p.name, f)
+
+
+def test_config3_full_second_matches_reference_golden(golden):
+    """BASELINE config 3 over its whole 1 s (10,000 steps, the bench's 256-step
+    windows in multi-window graphs): raster, counts, rates and every final
+    state array equal the reference's own run (golden cfg3_1000ms)."""
+    spec, mode = specs.config_spec(3, 1000.0)
+    sim = gpu_sim(spec, mode, window=256)
+    r = sim.finish()
+    assert_matches_golden_run(sim, r, spec, golden["runs"]["cfg3_1000ms"])
+
+
+@pytest.mark.parametrize("kw", [{}, {"virtualWorld": 8}])
+def test_config4_100ms_matches_reference_golden(golden, kw):
+    """BASELINE config 4 (1M KC) over 1,000 steps (four 256-step windows; the
+    arena-budgeted graph path), whole and as the 8-rank decomposition of §6
+    (virtual shards on one GPU): equal to the reference's own run."""
+    spec, mode = specs.config_spec(4, 100.0)
+    sim = gpu_sim(spec, mode, window=256, **kw)
+    r = sim.finish()
+    assert_matches_golden_run(sim, r, spec, golden["runs"]["cfg4_100ms"])
+
+
+@pytest.mark.parametrize("world", [1, 2, 8])
+def test_bench_split_networks_match_parity_golden(world):
+    """The networks bench.py times at N GPUs (N x 100k KC) over its 100-ms
+    parity horizon, split N ways (virtual shards): spike counts and the
+    order-independent raster checksum equal the reference's
+    (tests/golden/bench_parity.json)."""
+    import json
+    with open(os.path.join(os.path.dirname(__file__), "golden", "bench_parity.json")) as f:
+        gold = json.load(f)["runs"][f"split{world}"]
+    spec = specs.mbody_spec(100_000 * world, 0.05, 100.0)
+    kw = {"virtualWorld": world} if world > 1 else {}
+    sim = gpu_sim(spec, window=256, **kw)
+    r = sim.finish()
+    counts = [int(np.count_nonzero(r.raster.population == i)) for i in range(4)]
+    assert counts == gold["counts"]
+    assert specs.raster_checksum(r.raster.step, r.raster.population, r.raster.neuron) == \
+        int(gold["checksum"])
