@@ -388,8 +388,9 @@ RunResult run(const NetworkSpec& spec, StorageMode mode = StorageMode::FromSpec)
 RunResult run(const NetworkSpec& spec, StorageMode mode, const EngineOptions& options);
 
 // ---- calibration sweep (reference calibration.hpp:12-42), the hot path's caller ----
-// Cells run as independent device simulations driven by `parallelism` host
-// threads (each Simulation owns its streams, so cells overlap on the GPU).
+// Cells run as independent device simulations, up to `parallelism` in flight,
+// advanced round-robin by one host thread (each Simulation owns its streams,
+// so in-flight cells overlap on the GPU); specs are built on host threads ahead.
 
 struct SweepRow {
     std::int32_t nConn = 0;

@@ -93,6 +93,11 @@ def main():
     ap.add_argument("--launches-title", default="")
     ap.add_argument("--full")
     ap.add_argument("--full-title", default="")
+    ap.add_argument("--kc-metrics", help="ncu --csv --metrics log of the KC update launches "
+                    "(sm__inst_executed.sum, dram bytes, time) -> profiles/kc_update_ncu.json")
+    ap.add_argument("--kc-neurons", type=int, default=100_000)
+    ap.add_argument("--kc-steps", type=int, default=256)
+    ap.add_argument("--kc-source", default="")
     a = ap.parse_args()
     pdir = os.path.join(ROOT, "profiles")
     os.makedirs(pdir, exist_ok=True)
@@ -100,6 +105,29 @@ def main():
         per = launches(a.launches)
         with open(os.path.join(pdir, f"{a.round}_launches.txt"), "w") as f:
             f.write(launch_table(per, a.launches_title or f"ncu launch list ({a.launches})"))
+    if a.kc_metrics:
+        per = launches(a.kc_metrics)
+        kc = [d for d in per.values() if d["name"].startswith("condlif_window")
+              and int(d["grid"].strip("()").split(",")[0]) > 1]
+        inst = sorted(d["sm__inst_executed.sum"] for d in kc)
+        med = inst[len(inst) // 2]
+        rw = sorted(d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+                    for d in kc)
+        us = sorted(d.get("gpu__time_duration.sum", 0.0) for d in kc)
+        clk = [d.get("sm__cycles_elapsed.avg.per_second", 0.0) for d in kc]
+        out = {"round": a.round, "source": a.kc_source or os.path.basename(a.kc_metrics),
+               "kernel": "condlif_window_kernel (KC update, multi-block)", "launches": len(kc),
+               "neurons": a.kc_neurons, "steps_per_launch": a.kc_steps,
+               "warp_inst_per_launch_median": med,
+               "warp_inst_per_neuron_step": med / (a.kc_neurons * a.kc_steps),
+               "dram_bytes_per_launch": rw[len(rw) // 2],
+               "us_per_launch_median_cold_serialised": us[len(us) // 2],
+               "sm_mhz": (sum(clk) / len(clk) / 1e6) if clk and clk[0] else None,
+               "note": "sm__inst_executed.sum = warp instructions issued; bench.py's issue "
+                       "roofline scales warp_inst_per_neuron_step by the live launch's "
+                       "neuron-steps"}
+        with open(os.path.join(pdir, "kc_update_ncu.json"), "w") as f:
+            json.dump(out, f, indent=1)
     if a.full:
         rows = full_rows(a.full)
         lines = [a.full_title or f"ncu --set full ({a.full})", ""]
