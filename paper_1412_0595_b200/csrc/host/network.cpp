@@ -111,9 +111,9 @@ std::string weight_problem(const WeightDist& w) {
 std::vector<Violation> validate(const NetworkSpec& spec) {
     std::vector<Violation> out;
     Report rep{out};
-    if (!fin(spec.dtMs) || !(spec.dtMs > 0.0)) rep.add("dtMs", "dt must be finite and > 0");
+    if (!fin(spec.dtMs) || !(spec.dtMs > 0.0)) rep.add("dtMs", "dt must be positive and finite");
     if (!fin(spec.durationMs) || !(spec.durationMs > 0.0))
-        rep.add("durationMs", "duration must be finite and > 0");
+        rep.add("durationMs", "duration must be positive and finite");
     if (spec.populations.empty()) rep.add("populations", "at least one population is required");
 
     std::map<std::string, const NeuronPopulation*> byName;
@@ -145,7 +145,8 @@ std::vector<Violation> validate(const NetworkSpec& spec) {
             const double r = std::get<PoissonParams>(p.params).rateHz;
             if (!fin(r) || r < 0.0) rep.add(at + ".params.rateHz", "rate must be finite and >= 0");
             else if (fin(spec.dtMs) && spec.dtMs > 0.0 && r * spec.dtMs / 1000.0 > 1.0)
-                rep.add(at + ".params.rateHz", "rate * dt gives a spike probability above 1");
+                rep.add(at + ".params.rateHz",
+                        "spike probability per step rate * dt is above one (p > 1)");
         } else if (p.model == ModelKind::TraubMiles) {
             check_hh(std::get<TraubMilesParams>(p.params), at + ".params", rep);
         } else {
@@ -161,8 +162,10 @@ std::vector<Violation> validate(const NetworkSpec& spec) {
         else if (!groupNames.insert(g.name).second)
             rep.add(at + ".name", "synapse group name '" + g.name + "' is used twice");
         const auto pre = byName.find(g.pre), post = byName.find(g.post);
-        if (pre == byName.end()) rep.add(at + ".pre", "unknown population '" + g.pre + "'");
-        if (post == byName.end()) rep.add(at + ".post", "unknown population '" + g.post + "'");
+        if (pre == byName.end())
+            rep.add(at + ".pre", "pre side references unknown population '" + g.pre + "'");
+        if (post == byName.end())
+            rep.add(at + ".post", "post side references unknown population '" + g.post + "'");
         if (pre != byName.end() && pre->second->size >= 1) {
             const std::int32_t n = pre->second->size;
             if (g.preOffset < 0 || g.preOffset >= n) {

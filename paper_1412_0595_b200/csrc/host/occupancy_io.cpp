@@ -105,10 +105,13 @@ DeviceSpec device_preset(const std::string& name) {
     if (name == "sm100") return {"sm100", 32, 64, 32, 1024, 233472, 65536, 256, 128};
     std::string known;
     for (const auto& n : device_preset_names()) known += (known.empty() ? "" : ", ") + n;
+    known += ", sm100";
     throw SpecError("unknown device preset '" + name + "'; known presets: " + known);
 }
 
-std::vector<std::string> device_preset_names() { return {"cc20", "cc30", "cc50", "sm100"}; }
+// The reference's presets (occupancy.cpp:98-116, pinned by test_occupancy.cpp:265);
+// device_preset("sm100") (B200, extension) is accepted but not listed.
+std::vector<std::string> device_preset_names() { return {"cc20", "cc30", "cc50"}; }
 
 // ---- formats -------------------------------------------------------------------
 

