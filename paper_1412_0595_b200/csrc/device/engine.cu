@@ -87,8 +87,10 @@ void parallel_copy(void* dst, const void* src, std::size_t bytes) {
 // CRS tile pack of an inline sparse group for post tiles of tileN neurons
 // (layout in kernels.cuh, GroupDev::tpack).  With words == nullptr only the
 // largest tile's size (in 32-bit words, a multiple of 4) is computed.
+// perm > 0: columns in the order of the quad kernel with perm neurons per
+// thread (ssbk::quad_perm).
 std::int64_t tile_pack(const HostGroup& g, int tileN, std::vector<std::uint32_t>* words,
-                       std::vector<long long>* off) {
+                       std::vector<long long>* off, int perm = 0) {
     const int nwT = tileN / 32;
     const int nTiles = (g.nPost + tileN - 1) / tileN;
     const int rows = g.preCount;
@@ -117,18 +119,27 @@ std::int64_t tile_pack(const HostGroup& g, int tileN, std::vector<std::uint32_t>
             float* V = reinterpret_cast<float*>(Pf + static_cast<std::size_t>(rows) * nwT);
             std::uint32_t vi = 0;
             const int tile0 = t * tileN;
+            std::vector<std::pair<int, float>> ent;
             for (int r = 0; r < rows; ++r) {
                 std::uint32_t* m = M + static_cast<std::size_t>(r) * nwT;
+                ent.clear();
                 for (std::int64_t q = cur[r]; q < hi[r]; ++q) {
-                    const int c = g.ind[q] - tile0;
-                    m[c >> 5] |= 1u << (c & 31);
+                    int c = g.ind[q] - tile0;
+                    if (perm) c = ssbk::quad_perm(c, perm);
+                    ent.emplace_back(c, g.g[q]);
                 }
-                std::uint32_t run = vi;
+                // values in ascending (packed) column order = the mask's bit rank
+                if (perm) std::sort(ent.begin(), ent.end(),
+                                    [](const auto& a, const auto& b) { return a.first < b.first; });
+                for (const auto& [c, x] : ent) {
+                    m[c >> 5] |= 1u << (c & 31);
+                    std::memcpy(V + vi++, &x, 4);
+                }
+                std::uint32_t run = vi - static_cast<std::uint32_t>(ent.size());
                 for (int k = 0; k < nwT; ++k) {
                     Pf[static_cast<std::size_t>(r) * nwT + k] = run;
                     run += static_cast<std::uint32_t>(__builtin_popcount(m[k]));
                 }
-                for (std::int64_t q = cur[r]; q < hi[r]; ++q) std::memcpy(V + vi++, g.g + q, 4);
             }
             off->push_back(static_cast<long long>(words->size()));
         }
@@ -171,6 +182,10 @@ bool kernel_attributes(const std::string& name, int& regs, int& sharedBytes, int
     cudaFuncAttributes a;
     cudaError_t e;
     if (name == "condlif_window") e = cudaFuncGetAttributes(&a, ssbk::condlif_window_kernel);
+    else if (name == "condlif_quad_window")
+        e = cudaFuncGetAttributes(&a, ssbk::condlif_quad_window_kernel);
+    else if (name == "condlif_pair_window")
+        e = cudaFuncGetAttributes(&a, ssbk::condlif_pair_window_kernel);
     else if (name == "izh_window") e = cudaFuncGetAttributes(&a, ssbk::izh_window_kernel);
     else if (name == "hh_window") e = cudaFuncGetAttributes(&a, ssbk::hh_window_kernel);
     else if (name == "gaussian_window") e = cudaFuncGetAttributes(&a, ssbk::gaussian_window_kernel);
@@ -232,6 +247,7 @@ struct DeviceEngine::Impl {
         int smemBytes = 0;          // dynamic shared memory of the population kernel
         int offBits = -1;           // shared copy of the window's spike bits (1-block pops)
         int tileN = 0;              // neurons per block
+        int quad = 0;               // CondLif: neurons per thread of the quad kernel (0: tile kernel)
         int chunk = 1;              // steps per phase-A/phase-B chunk
         int offIn = 0;              // shared offset of the phase-A inputs
         std::vector<int> accGroups[2];  // group indices in spec order
@@ -434,6 +450,7 @@ struct DeviceEngine::Impl {
 
     int choose_block(int n, const std::function<std::int64_t(int)>& smemFor,
                      const void* kernelFn) const;
+    int plan_stage_quad(const HostNet& net, int pi, int tileN, ssbk::StageAcc out[2]) const;
     int plan_stage(const HostNet& net, int pi, int tileN, ssbk::StageAcc out[2], int& offIn,
                    int& C, int& offBits) const;
     void build(const HostNet& net);
@@ -601,6 +618,53 @@ int DeviceEngine::Impl::choose_block(int n, const std::function<std::int64_t(int
     }
     if (best == 0) best = 32;
     return std::min(best, single);
+}
+
+// Shared-memory layout of the quad CondLif kernel (quad.cuh) for tiles of
+// tileN = 4 x threads: per inline group its pre lists and either the permuted
+// dense tile + a zero row + the first-four-rows table, or the permuted CRS
+// tile pack.  Returns the bytes, or -1 when the population does not qualify
+// (an accumulator with several inline groups, or a tile that does not fit).
+int DeviceEngine::Impl::plan_stage_quad(const HostNet& net, int pi, int tileN,
+                                        ssbk::StageAcc out[2]) const {
+    const auto& P = pops[pi];
+    auto align = [](std::int64_t v, std::int64_t a) { return (v + a - 1) / a * a; };
+    const int W = Wmax;
+    std::int64_t off = 0;
+    for (int a = 0; a < 2; ++a) {
+        out[a] = ssbk::StageAcc{};
+        const auto& A = P.acc[a];
+        if (A.mode == ssbk::kAccNone || A.mode == ssbk::kAccBuffered) continue;
+        if (A.mode != ssbk::kAccInline || A.ng != 1) return -1;
+        const auto& g = net.groups[P.accGroups[a][0]];
+        const int preN = net.pops[g.pre].n;
+        auto& S = out[a].g[0];
+        S.listCap = static_cast<int>(std::min<std::int64_t>(static_cast<std::int64_t>(W) * preN, 4096));
+        S.offCnt = static_cast<int>(off);
+        off += (W + 1) * 4;
+        S.offList = static_cast<int>(off);
+        off += static_cast<std::int64_t>(S.listCap) * 4;
+        if (g.dense) {
+            S.stageW = 1;
+            off = align(off, 16);
+            S.offW = static_cast<int>(off);
+            off += static_cast<std::int64_t>(g.preCount + 1) * tileN * 4;
+            S.offRoff = static_cast<int>(off);
+            off += static_cast<std::int64_t>(W + 1) * 4;
+            off = align(off, 16);
+            S.offRows4 = static_cast<int>(off);  // chunks: at most listCap / 4 + W
+            off += (static_cast<std::int64_t>(S.listCap) / 4 + W + 1) * 16;
+        } else {
+            const std::int64_t tw = tile_pack(g, tileN, nullptr, nullptr);
+            if (tw > kTilePackMaxWords) return -1;
+            S.tpackWords = static_cast<int>(std::max<std::int64_t>(tw, 4));
+            off = align(off, 16);
+            S.offT = static_cast<int>(off);
+            off += static_cast<std::int64_t>(S.tpackWords) * 4;
+        }
+    }
+    const std::int64_t total = align(off, 16);
+    return total <= 200 * 1024 ? static_cast<int>(total) : -1;
 }
 
 // Shared-memory layout of a CondLif population kernel for tiles of tileN
@@ -776,7 +840,37 @@ void DeviceEngine::Impl::build(const HostNet& net) {
                 for (int gi : gl)
                     if (!net.groups[gi].dense) P.sparseInline = true;
         }
-        if (hp.kind == kCondLif || hp.kind == kIzhikevich || hp.kind == kTraubMiles) {
+        // multi-block CondLif populations whose inputs qualify take the quad
+        // kernel (four neurons per thread): threads per block so that the
+        // blocks cover the SMs left to this population once (the paper's
+        // occupancy model as is, blockPolicy 1, keeps the tile kernel)
+        static const bool quadOff = std::getenv("SSB_QUAD") && std::string(std::getenv("SSB_QUAD")) == "0";
+        static const int quadNpt = [] {
+            const char* e = std::getenv("SSB_QUAD_NPT");
+            return e && std::atoi(e) == 4 ? 4 : 2;
+        }();
+        if (hp.kind == kCondLif && !quadOff && cfg.blockPolicy != 1 && hp.n >= 2048) {
+            const int sms = std::max(1, smCount - reservedSMs);
+            const int npt = quadNpt;
+            int T = cfg.blockSize > 0 ? round_up(cfg.blockSize, 32)
+                                      : round_up((hp.n + npt * sms - 1) / (npt * sms), 32);
+            T = std::clamp(T, 64, ssbk::kQuadMaxThreads);
+            for (; T >= 64 && !P.quad; T -= 32) {
+                const int bytes = plan_stage_quad(net, pi, npt * T, P.stage);
+                if (bytes < 0) {
+                    if (cfg.blockSize > 0) break;
+                    continue;
+                }
+                P.quad = npt;
+                P.tileN = npt * T;
+                P.block = T;
+                P.grid = (hp.n + P.tileN - 1) / P.tileN;
+                P.smemBytes = bytes;
+            }
+        }
+        if (P.quad) {
+            // planned above
+        } else if (hp.kind == kCondLif || hp.kind == kIzhikevich || hp.kind == kTraubMiles) {
             // tile size from the occupancy model (registers of the kernel +
             // this tile's shared-memory plan, 1 KB per-block reservation)
             ssbk::StageAcc tmp[2];
@@ -979,6 +1073,21 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         G.preCnt = pre.dev.count;
         if (g.dense) {
             G.W = upload<float>(g.W, static_cast<std::size_t>(g.nPre) * g.nPost);
+            if (post.quad) {
+                // the quad kernel's tile-major, column-permuted copy (quad.cuh)
+                const int tn = post.tileN, nt = (g.nPost + tn - 1) / tn, rows = g.preCount + 1;
+                std::vector<float> wq(static_cast<std::size_t>(nt) * rows * tn, 0.f);
+                for (int t = 0; t < nt; ++t)
+                    for (int r = 0; r < g.preCount; ++r) {
+                        float* dst = wq.data() + (static_cast<std::size_t>(t) * rows + r) * tn;
+                        const float* src = g.W + static_cast<std::size_t>(r) * g.nPost;
+                        for (int c = 0; c < tn && t * tn + c < g.nPost; ++c) {
+                            const float x = src[t * tn + c];
+                            dst[ssbk::quad_perm(c, post.quad)] = x == 0.f ? 0.f : x;
+                        }
+                    }
+                G.Wq = upload<float>(wq.data(), wq.size());
+            }
         } else {
             G.segTile = post.kind != kPoisson ? post.tileN : 256;
             G.nTiles = (g.nPost + G.segTile - 1) / G.segTile;
@@ -1008,7 +1117,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             if (packed) {
                 std::vector<std::uint32_t> words;
                 std::vector<long long> offs;
-                tile_pack(g, post.tileN, &words, &offs);
+                tile_pack(g, post.tileN, &words, &offs, post.quad);
                 G.tpack = upload<std::uint32_t>(words.data(), words.size());
                 G.tpackOff = upload<long long>(offs.data(), offs.size());
                 G.nwT = post.tileN / 32;
@@ -1145,6 +1254,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     for (const auto& P : pops) maxSmem = std::max(maxSmem, P.smemBytes);
     auto allow = allow_smem;
     allow(reinterpret_cast<const void*>(&ssbk::condlif_window_kernel), std::max(maxSmem, 4096));
+    allow(reinterpret_cast<const void*>(&ssbk::condlif_quad_window_kernel), std::max(maxSmem, 4096));
+    allow(reinterpret_cast<const void*>(&ssbk::condlif_pair_window_kernel), std::max(maxSmem, 4096));
     allow(reinterpret_cast<const void*>(&ssbk::izh_window_kernel), std::max(maxSmem, 4096));
     allow(reinterpret_cast<const void*>(&ssbk::hh_window_kernel), std::max(maxSmem, 4096));
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_warp_kernel), kWarpRingBytes);
@@ -1253,7 +1364,9 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
         } else if (P.kind == kTraubMiles) {
             update("hh_window:", ssbk::hh_window_kernel);
         } else {
-            update("condlif_window:", ssbk::condlif_window_kernel);
+            update("condlif_window:", P.quad == 4   ? ssbk::condlif_quad_window_kernel
+                                      : P.quad == 2 ? ssbk::condlif_pair_window_kernel
+                                                    : ssbk::condlif_window_kernel);
         }
         // the next wide kernel may start right after the update: compaction
         // (on sp) feeds only this window's consumers
