@@ -1,5 +1,7 @@
 // engine.cu — DeviceEngine: device memory layout, launch schedule, CUDA
 // graphs and raster management of the windowed step engine.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <sys/mman.h>
 
@@ -44,6 +46,35 @@ void allow_smem(const void* fn, int bytes) {
     CK(cudaFuncGetAttributes(&fa, fn));
     if (fa.maxDynamicSharedSizeBytes < bytes)
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+// Tensor map of a dense group's weights [preCount][nPost] (fp32, row-major)
+// for TMA row gathers: box = one whole row, out-of-range rows read as +0.
+// cuTensorMapEncodeTiled is a driver entry point (the library links cudart
+// statically and never links libcuda).  False when unavailable.
+bool encode_row_tmap(CUtensorMap* tm, const float* w, int rows, int cols, int boxCols = 0,
+                     int boxRows = 1) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+        }
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode || rows < 1 || cols < 4 || cols > 256 || cols % 4) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 4};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(boxCols > 0 ? boxCols : cols),
+                               static_cast<cuuint32_t>(boxRows)};
+    const cuuint32_t elem[2] = {1, 1};
+    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(w), dims, strides, box,
+                  elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Host store of drained raster events: anonymous mappings with transparent
@@ -529,9 +560,42 @@ struct DeviceEngine::Impl {
     // warp per step with a per-lane cp.async ring; SSB_DENSE_KERNEL=pipe
     // selects the block-per-step ring), plain coalesced gathers otherwise.
     bool usePipe = false;
+    // heavy dense groups: the cp.async chain kernel by default; SSB_DENSE_KERNEL=
+    // tma (TMA gather4 rows), ldg (rows through registers) or rowstream (the
+    // matrix streamed in row order) select the experimental gathers of
+    // gather_tma.cuh (all bit-exact; slower at config 3)
+    bool useTmaGather = false;
+    bool useLdgGather = false;
+    std::vector<CUtensorMap> rowTmaps;  // per group (heavy dense groups; see hasRowTmap)
+    std::vector<char> hasRowTmap;
+    std::vector<CUtensorMap> tileTmaps;  // per group: 256-row x 8-column boxes (row streaming)
+    bool useRowStream = false;
     void launch_dense(const ssbk::GroupDev& G, const std::string& gname, const char* tag,
-                      float* out, long long stride, int wLo, int nW, int first, cudaStream_t s) {
-        if (G.nPost % 4 == 0 && G.nPost <= ssbk::kChainMaxPost && !usePipe) {
+                      float* out, long long stride, int wLo, int nW, int first, cudaStream_t s,
+                      const CUtensorMap* tm = nullptr, const CUtensorMap* tileTm = nullptr) {
+        if (tileTm && useRowStream) {
+            // the matrix streamed once in row order, every step taking its rows
+            const dim3 grid((G.nPost + ssbk::kRsCols - 1) / ssbk::kRsCols,
+                            (nW + ssbk::kRsThreads - 1) / ssbk::kRsThreads);
+            launch(std::string(tag) + gname, [&] {
+                ssbk::dense_window_rowstream_kernel<<<grid, ssbk::kRsThreads, ssbk::kRsSmem, s>>>(
+                    *tileTm, G, out, stride, wLo, nW, first);
+            });
+        } else if (tm && useLdgGather) {
+            // rows through registers, one warp per window step (gather_tma.cuh)
+            const int blocks = (nW + 7) / 8;
+            launch(std::string(tag) + gname, [&] {
+                ssbk::dense_window_ldg_kernel<<<blocks, 256, 0, s>>>(G, out, stride, wLo, nW, first);
+            });
+        } else if (tm && useTmaGather) {
+            // TMA row gathers, one warp per window step (gather_tma.cuh)
+            const int blocks = (nW + ssbk::kTmaWarps - 1) / ssbk::kTmaWarps;
+            const int smem = ssbk::tma_smem_bytes(G.nPost);
+            launch(std::string(tag) + gname, [&] {
+                ssbk::dense_window_tma_kernel<<<blocks, 32 * ssbk::kTmaWarps, smem, s>>>(
+                    *tm, G, out, stride, wLo, nW, first);
+            });
+        } else if (G.nPost % 4 == 0 && G.nPost <= ssbk::kChainMaxPost && !usePipe) {
             const int cw = G.nPost * chain_steps(G.nPost);  // stage row width
             const int smem = ssbk::kChainStages * ssbk::kChainPer * (ssbk::kChainCopiers / (cw / 4)) *
                              cw * 4;
@@ -639,7 +703,9 @@ int DeviceEngine::Impl::plan_stage_quad(const HostNet& net, int pi, int tileN,
         const auto& g = net.groups[P.accGroups[a][0]];
         const int preN = net.pops[g.pre].n;
         auto& S = out[a].g[0];
-        S.listCap = static_cast<int>(std::min<std::int64_t>(static_cast<std::int64_t>(W) * preN, 4096));
+        // (a window whose lists overflow reads them from global memory; 2048
+        // keeps a KC block at ~131 KB so a kc_dn gather block fits beside it)
+        S.listCap = static_cast<int>(std::min<std::int64_t>(static_cast<std::int64_t>(W) * preN, 2048));
         S.offCnt = static_cast<int>(off);
         off += (W + 1) * 4;
         S.offList = static_cast<int>(off);
@@ -850,7 +916,15 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             return e && std::atoi(e) == 4 ? 4 : 2;
         }();
         if (hp.kind == kCondLif && !quadOff && cfg.blockPolicy != 1 && hp.n >= 2048) {
-            const int sms = std::max(1, smCount - reservedSMs);
+            // a quarter of the SMs stay free for the other populations and the
+            // heavy gathers (kc_dn), which otherwise take SMs the next window's
+            // update waits for (device trace: 14 reserved SMs -> KC blocks up
+            // to 26 us late, window 97 us; 37 -> ~4 us, 91 us)
+            static const int quadReserved = [&] {
+                const char* e = std::getenv("SSB_RESERVED_SMS");
+                return e ? std::atoi(e) : smCount / 4;
+            }();
+            const int sms = std::max(1, smCount - (nPops > 1 && !stepMode ? quadReserved : 0));
             const int npt = quadNpt;
             int T = cfg.blockSize > 0 ? round_up(cfg.blockSize, 32)
                                       : round_up((hp.n + npt * sms - 1) / (npt * sms), 32);
@@ -1073,6 +1147,16 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         G.preCnt = pre.dev.count;
         if (g.dense) {
             G.W = upload<float>(g.W, static_cast<std::size_t>(g.nPre) * g.nPost);
+            // TMA row gathers for wide-enough groups (launch_dense)
+            if (rowTmaps.empty()) {
+                rowTmaps.resize(net.groups.size());
+                hasRowTmap.assign(net.groups.size(), 0);
+            }
+            if (tileTmaps.empty()) tileTmaps.resize(net.groups.size());
+            if (g.nPost % 4 == 0 && g.nPost >= 32 && g.nPost <= ssbk::kChainMaxPost)
+                hasRowTmap[gi] = encode_row_tmap(&rowTmaps[gi], G.W, g.preCount, g.nPost) &&
+                                 encode_row_tmap(&tileTmaps[gi], G.W, g.preCount, g.nPost,
+                                                 ssbk::kRsCols, ssbk::kRsBox);
             if (post.quad) {
                 // the quad kernel's tile-major, column-permuted copy (quad.cuh)
                 const int tn = post.tileN, nt = (g.nPost + tn - 1) / tn, rows = g.preCount + 1;
@@ -1262,7 +1346,16 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     allow(reinterpret_cast<const void*>(&ssbk::dense_window_pipe_kernel), ring_smem());
     for (int np = 4; np <= ssbk::kChainMaxPost; np += 4)
         allow(reinterpret_cast<const void*>(chain_kernel(np)), ssbk::kChainSmem);
-    if (const char* e = std::getenv("SSB_DENSE_KERNEL")) usePipe = std::string(e) == "pipe";
+    if (const char* e = std::getenv("SSB_DENSE_KERNEL")) {
+        const std::string k = e;
+        usePipe = k == "pipe";
+        useTmaGather = k == "tma";
+        useLdgGather = k == "ldg";
+        useRowStream = k == "rowstream";
+    }
+    allow(reinterpret_cast<const void*>(&ssbk::dense_window_rowstream_kernel), ssbk::kRsSmem);
+    allow(reinterpret_cast<const void*>(&ssbk::dense_window_tma_kernel),
+          ssbk::tma_smem_bytes(ssbk::kChainMaxPost));
     if (const char* e = std::getenv("SSB_TIMELINE")) timelinePath = e;
     if (const char* e = std::getenv("SSB_TRACE")) {  // per-block trace (scripts/trace_kc.py)
         tracePath = e;
@@ -1307,7 +1400,12 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
                 if (G.dense || G.fullRows) {
                     ssbk::GroupDev D = G;
                     if (!G.dense) D.W = G.g;  // full CRS rows = dense rows
-                    launch_dense(D, groupMeta[gi].name, "dense_window:", out, P.n, 1, W, k == 0, sg);
+                    const CUtensorMap* tm =
+                        G.dense && gi < static_cast<int>(hasRowTmap.size()) && hasRowTmap[gi]
+                            ? &rowTmaps[gi]
+                            : nullptr;
+                    launch_dense(D, groupMeta[gi].name, "dense_window:", out, P.n, 1, W, k == 0, sg,
+                                 tm, tm ? &tileTmaps[gi] : nullptr);
                 } else {
                     dim3 grid(G.nTiles, W);
                     launch("sparse_window:" + groupMeta[gi].name, [&] {

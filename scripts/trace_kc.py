@@ -38,7 +38,7 @@ base = t0.min()
 t0, t1 = (t0 - base) / 1e3, (t1 - base) / 1e3  # us
 nkc = 100_000 * max(1, emu) // max(1, emu) if emu <= 1 else None
 kc_tag = max(int(x) for x in set(tag.tolist()) if x < 0xfffffff0)
-names = {kc_tag: "kc", 20: "lhi", 100: "dn", 0xffffffff: "kc_dn", 0xfffffffd: "raster"}
+names = {kc_tag: "kc", 20: "lhi", 100: "dn", 0xffffffff: "kc_dn", 0xfffffffc: "kc_dn(tma)", 0xfffffffd: "raster"}
 if emu > 1:
     names[16] = "dn (local slice)"
 # the last nwin windows' KC launches: split KC blocks into launches by start gaps
