@@ -151,7 +151,8 @@ typedef struct ssb_engine_opts {
     int32_t block_policy;        /* 0 = occupancy model + SM fill, 1 = paper model only */
     int32_t use_graphs;          /* 0 = default (on), 1 = on, -1 = off */
     int32_t heavy_pre_threshold; /* groups with >= this many pre rows use the buffered path */
-    int64_t raster_capacity;     /* events kept on device between host flushes */
+    int64_t raster_capacity;     /* raster bitmask words kept on device between host flushes
+                                  * (at least two graph launches of windows) */
     int32_t profile;             /* 1 = time every launch with CUDA events */
     int32_t force_step_mode;     /* 1 = never fuse steps (window forced to 1) */
     /* multi-GPU: one process per GPU, rank of world_size, NCCL

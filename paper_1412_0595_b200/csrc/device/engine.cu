@@ -341,17 +341,24 @@ struct DeviceEngine::Impl {
     std::int64_t stepsDone = 0;
     std::int64_t windowsLaunched = 0;
 
-    // raster: the device arena is flushed to the host only when it may be
-    // near full.  The cursor after each window is copied asynchronously to a
-    // pinned ring; the host never runs more than kRing windows ahead, so the
-    // arena fill is known up to kRing windows of worst-case growth.
-    static constexpr int kRing = 2;
+    // raster: the device arena records each window's spike bitmask rows (a
+    // fixed rowWords words per step, kernels.cuh RasterDev), so the host knows
+    // its fill exactly and flushes it only when the next launch would not
+    // fit; a flush decodes the rows into events on the device (copy stream)
+    // and moves them to host memory while the simulation fills the other arena.
     ssbk::RasterDev raster{};
-    std::int64_t rasterCap = 0;
-    long long* ringVal = nullptr;  // pinned
-    cudaEvent_t ringEv[kRing] = {};
-    std::int64_t ringAdd[kRing] = {};
-    std::int64_t knownCursor = 0, knownWin = 0, epochStart = 0;
+    std::int64_t rasterCap = 0;      // words per arena
+    std::int64_t cursorHost = 0;     // words recorded in the active arena
+    std::int64_t arenaStep0 = 0;     // first step recorded in the active arena
+    std::vector<int> arenaWins;      // window sizes recorded in the active arena
+    static constexpr std::size_t kEvStage = std::size_t(1) << 24;  // decoded events per chunk
+    std::size_t evStageCap = 0;
+    int* evStage = nullptr;          // device: decoded events of one chunk
+    long long* rowOffDev = nullptr;  // device: arena offset of each drained step
+    long long* evOffDev = nullptr;   // device: event offset of each (step, pop)
+    std::int64_t maxArenaSteps = 0;
+    cudaEvent_t flushEv = nullptr;       // recorded on the stream when an arena is switched out
+    long long* pinnedConst = nullptr;    // pinned {0, 1, 0}: arena selector values, zero cursor
     bool rasterDiscarded = false;
     // Host copy of the raster: drained arenas, in order.  A flush switches the
     // device to the other arena and drains the full one on a copy stream from
@@ -978,22 +985,21 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     if (const char* e = std::getenv(stepMode ? "SSB_STEP_GRAPH_WINDOWS" : "SSB_GRAPH_WINDOWS"))
         graphWindows = std::clamp(std::atoi(e), 1, kMaxSets);
     {
-        // The host runs at most kRing launches ahead of the last cursor it has
-        // seen, so the arena must hold kRing + 1 launches of worst-case events
-        // (every neuron spiking every step).  The two arenas may take 4G events
-        // each or 30% of the device memory free now, whichever is more (a
-        // split world's every rank records the global raster: at 8 x 100k KC
-        // a 4G cap allowed 6 windows per launch and each graph boundary cost
-        // ~100 us per window); beyond that the launch shrinks.
+        // Every window of a launch has its own window-buffer set (spike lists
+        // [W][n] per population, the global ones too for split populations);
+        // the sets of one launch may take 25% of the device memory free now
+        // (the raster arena is fixed-size bitmask rows, see flush_raster).
         std::size_t freeB = 0, totalB = 0;
         if (cudaMemGetInfo(&freeB, &totalB) != cudaSuccess) {
             cudaGetLastError();
             freeB = 0;
         }
-        const std::int64_t budget = std::max<std::int64_t>(
-            std::int64_t(1) << 32, static_cast<std::int64_t>(0.30 * static_cast<double>(freeB)) / 8);
-        const std::int64_t perWin = static_cast<std::int64_t>(Wmax) * totalNeurons;
-        const std::int64_t fit = budget / ((kRing + 1) * std::max<std::int64_t>(perWin, 1));
+        std::int64_t perSet = 0;
+        for (const auto& P : pops)
+            perSet += static_cast<std::int64_t>(Wmax) * 4 *
+                      (P.n + (P.sharded ? P.nGlobal : 0) + 2 * (P.nwords + P.nwGlobal));
+        const std::int64_t budget = static_cast<std::int64_t>(0.25 * static_cast<double>(freeB));
+        const std::int64_t fit = budget / std::max<std::int64_t>(perSet, 1);
         graphWindows = static_cast<int>(std::clamp<std::int64_t>(fit, 1, graphWindows));
     }
     nSets = std::clamp(graphWindows, 2, kMaxSets);
@@ -1273,30 +1279,57 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         const auto& P = pops[pi];
         r.n[pi] = P.nGlobal;
         r.add[pi] = 0;
-        r.count[pi] = P.devb[b].count;
-        r.list[pi] = P.devb[b].list;
+        r.bits[pi] = P.devb[b].bits;
+        r.nw[pi] = P.sharded ? P.nwGlobal : P.nwords;
         if (!rasterLocal) return;
         if (P.sharded) {
             r.n[pi] = P.n;
             r.add[pi] = P.lo;
-            r.count[pi] = P.kdev[b].count;
-            r.list[pi] = P.kdev[b].list;
+            r.bits[pi] = P.kdev[b].bits;
+            r.nw[pi] = P.nwords;
         } else if (cfg.rank != 0) {
-            r.count[pi] = zeroCounts;
+            r.bits[pi] = nullptr;  // recorded by rank 0
         }
     };
     for (int pi = 0; pi < nPops; ++pi) raster_src(raster, pi, 0);
-    // raster arena capacity for kRing + 1 launches of worst-case events
-    const std::int64_t perWindow = static_cast<std::int64_t>(Wmax) * totalNeurons;
-    const std::int64_t perLaunch = perWindow * graphWindows;
-    rasterCap = cfg.rasterCapacity > 0
-                    ? cfg.rasterCapacity
-                    : std::max<std::int64_t>(std::int64_t(1) << 26, (kRing + 1) * perLaunch);
-    rasterCap = std::max(rasterCap, (kRing + 1) * perLaunch);
-    CK(cudaMallocHost(&ringVal, kRing * sizeof(long long)));
-    for (auto& e : ringEv) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    raster.rowWords = 0;
+    for (int pi = 0; pi < nPops; ++pi) {
+        raster.popOff[pi] = raster.rowWords;
+        raster.rowWords += raster.nw[pi];
+    }
+    // arena (words): 2% of the device memory (config 3 on a B200: ~29
+    // simulated seconds, so a run's raster stays on the device until it is
+    // drained or collected, as in the device-timed bench), at least two
+    // launches of windows; rasterCapacity overrides it.  The fill never
+    // depends on the activity.
+    const std::int64_t perLaunch =
+        static_cast<std::int64_t>(Wmax) * graphWindows * std::max(raster.rowWords, 1);
+    std::int64_t capDefault = 0;
+    {
+        std::size_t freeB = 0, totalB = 0;
+        if (cudaMemGetInfo(&freeB, &totalB) == cudaSuccess)
+            capDefault = static_cast<std::int64_t>(0.02 * static_cast<double>(totalB)) / 4;
+        else
+            cudaGetLastError();
+        // and never more than the whole run needs
+        capDefault = std::min<std::int64_t>(
+            capDefault, (stepsTotal + static_cast<std::int64_t>(Wmax) * graphWindows) *
+                            std::max(raster.rowWords, 1));
+    }
+    rasterCap = std::max<std::int64_t>(cfg.rasterCapacity > 0 ? cfg.rasterCapacity : capDefault,
+                                       2 * perLaunch);
+    maxArenaSteps = rasterCap / std::max(raster.rowWords, 1) + 1;
     raster.arena[0] = alloc<int>(static_cast<std::size_t>(rasterCap), false);
     raster.arena[1] = alloc<int>(static_cast<std::size_t>(rasterCap), false);
+    evStageCap = kEvStage;
+    evStage = alloc<int>(evStageCap, false);
+    CK(cudaEventCreateWithFlags(&flushEv, cudaEventDisableTiming));
+    CK(cudaMallocHost(&pinnedConst, 4 * sizeof(long long)));
+    pinnedConst[0] = 0;
+    pinnedConst[1] = 1;
+    pinnedConst[2] = 0;
+    rowOffDev = alloc<long long>(static_cast<std::size_t>(maxArenaSteps), false);
+    evOffDev = alloc<long long>(static_cast<std::size_t>(maxArenaSteps) * nPops, false);
     arenaSelDev = alloc<int>(1);
     raster.arenaSel = arenaSelDev;
     CK(cudaStreamCreateWithFlags(&copyStream, cudaStreamNonBlocking));
@@ -1648,109 +1681,162 @@ void DeviceEngine::Impl::enqueue_windows(int W, int M) {
 }
 
 // Switches the device to the other arena and drains the full one in the
-// background (wait = true: drain synchronously, e.g. to collect results).
+// background (wait = true: drain synchronously, e.g. to collect results): the
+// recorded bitmask rows are decoded into events on the device (copy stream,
+// chunks of at most kEvStage events) and copied to host memory -- straight
+// into the pinned pool's blocks when enough are free, else through pinned
+// staging into huge-page host memory.
 void DeviceEngine::Impl::flush_raster(bool wait) {
-    CK(cudaStreamSynchronize(stream));
-    long long cur = 0;
-    const int parity = static_cast<int>(windowsLaunched & 1);
-    CK(cudaMemcpy(&cur, raster.cursor + parity, sizeof(long long), cudaMemcpyDeviceToHost));
+    // the switch is enqueued on the stream (no host wait): windows enqueued
+    // before it fill the full arena, later ones the other; the drain waits
+    // for flushEv, recorded right after the switch
     join_copier();  // the other arena must be drained before it is reused
+    const int parity = static_cast<int>(windowsLaunched & 1);
     const int full = arenaSel;
     arenaSel ^= 1;
-    CK(cudaMemcpy(arenaSelDev, &arenaSel, sizeof(int), cudaMemcpyHostToDevice));
-    std::vector<std::int32_t*> blocks;
-    if (cur > 0 && !rasterDiscarded && pinPool) {
-        const std::size_t need = (static_cast<std::size_t>(cur) + kPoolBlockInts - 1) / kPoolBlockInts;
-        std::lock_guard<std::mutex> lk(pinPool->mu);
-        if (pinPool->free.size() >= need) {
-            blocks.assign(pinPool->free.end() - need, pinPool->free.end());
-            pinPool->free.resize(pinPool->free.size() - need);
-        }
+    // pinnedConst holds 0 and 1 as long longs: their low words are the int selector
+    CK(cudaMemcpyAsync(arenaSelDev, reinterpret_cast<const int*>(pinnedConst + arenaSel),
+                       sizeof(int), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(raster.cursor + parity, pinnedConst + 2, sizeof(long long),
+                       cudaMemcpyHostToDevice, stream));
+    CK(cudaEventRecord(flushEv, stream));
+    auto wins = std::make_shared<std::vector<int>>();
+    wins->swap(arenaWins);
+    const std::int64_t step0 = arenaStep0;
+    arenaStep0 = stepsDone;
+    cursorHost = 0;
+    if (wins->empty() || rasterDiscarded) {
+        if (wait) CK(cudaEventSynchronize(flushEv));
+        return;
     }
-    if (!blocks.empty()) {  // straight into pinned pool blocks
-        const int* src = raster.arena[full];
-        const std::size_t total = static_cast<std::size_t>(cur);
-        std::shared_ptr<PinnedPool> pool = pinPool;
-        for (std::size_t i = 0; i < blocks.size(); ++i) {
-            const std::size_t len = std::min(kPoolBlockInts, total - i * kPoolBlockInts);
-            hostChunks.emplace_back(std::shared_ptr<std::int32_t>(blocks[i], [pool](std::int32_t* q) {
-                                        std::lock_guard<std::mutex> lk(pool->mu);
-                                        pool->free.push_back(q);
-                                    }),
-                                    len);
+    const int nP = raster.nPops;
+    const int dev = cfg.device;
+    cudaStream_t cs = copyStream;
+    cudaEvent_t ready = flushEv;
+    std::int32_t* stage[2] = {pinned[0], pinned[1]};
+    const uint32_t* arena = reinterpret_cast<const uint32_t*>(raster.arena[full]);
+    const ssbk::RasterDev R = raster;
+    int* ev = evStage;
+    const std::size_t evCap = evStageCap;
+    long long* rowD = rowOffDev;
+    long long* evD = evOffDev;
+    const int* countsDev = raster.countsAll + step0 * nP;
+    std::shared_ptr<PinnedPool> pool = pinPool;
+    auto* chunks = &hostChunks;
+    auto drain = [=] {
+        cudaSetDevice(dev);
+        cudaEventSynchronize(ready);
+        // per-step arena offsets and per-(step, pop) event offsets
+        std::int64_t nSteps = 0;
+        for (int w : *wins) nSteps += w;
+        std::vector<int> cnt(static_cast<std::size_t>(nSteps) * nP);
+        cudaMemcpyAsync(cnt.data(), countsDev, cnt.size() * 4, cudaMemcpyDeviceToHost, cs);
+        cudaStreamSynchronize(cs);
+        std::vector<long long> rowOff(static_cast<std::size_t>(nSteps)), evOff(cnt.size() + 1);
+        std::size_t total = 0;
+        std::vector<std::int64_t> cuts{0};  // chunks of steps whose events fit the stage
+        std::size_t acc = 0;
+        for (std::int64_t st = 0; st < nSteps; ++st) {
+            rowOff[st] = st * R.rowWords;
+            std::size_t e = 0;
+            for (int p = 0; p < nP; ++p) {
+                evOff[st * nP + p] = static_cast<long long>(total);
+                total += static_cast<std::size_t>(cnt[st * nP + p]);
+                e += static_cast<std::size_t>(cnt[st * nP + p]);
+            }
+            if (acc + e > evCap && st > 0) {
+                cuts.push_back(st);
+                acc = 0;
+            }
+            acc += e;
         }
-        const int dev = cfg.device;
-        cudaStream_t cs = copyStream;
-        auto drain = [blocks, src, total, dev, cs] {
-            cudaSetDevice(dev);
-            for (std::size_t i = 0; i < blocks.size(); ++i) {
-                const std::size_t off = i * kPoolBlockInts;
-                cudaMemcpyAsync(blocks[i], src + off, std::min(kPoolBlockInts, total - off) * 4,
-                                cudaMemcpyDeviceToHost, cs);
+        evOff[cnt.size()] = static_cast<long long>(total);
+        cuts.push_back(nSteps);
+        if (total == 0) return;
+        // destination segments (host memory, in event order)
+        std::vector<std::pair<std::int32_t*, std::size_t>> segs;
+        bool pooled = false;
+        if (pool) {
+            const std::size_t need = (total + kPoolBlockInts - 1) / kPoolBlockInts;
+            std::lock_guard<std::mutex> lk(pool->mu);
+            if (pool->free.size() >= need) {
+                std::vector<std::int32_t*> blocks(pool->free.end() - need, pool->free.end());
+                pool->free.resize(pool->free.size() - need);
+                for (std::size_t i = 0; i < blocks.size(); ++i) {
+                    const std::size_t len = std::min(kPoolBlockInts, total - i * kPoolBlockInts);
+                    chunks->emplace_back(std::shared_ptr<std::int32_t>(blocks[i], [pool](std::int32_t* q) {
+                                             std::lock_guard<std::mutex> lk2(pool->mu);
+                                             pool->free.push_back(q);
+                                         }),
+                                         len);
+                    segs.emplace_back(blocks[i], len);
+                }
+                pooled = true;
             }
-            cudaStreamSynchronize(cs);
-        };
-        if (wait) drain();
-        else copier = std::thread(drain);
-    } else if (cur > 0 && !rasterDiscarded) {
-        auto chunk = host_events(static_cast<std::size_t>(cur));
-        std::int32_t* dst = chunk.get();
-        hostChunks.emplace_back(std::move(chunk), static_cast<std::size_t>(cur));
-        const int* src = raster.arena[full];
-        const int dev = cfg.device;
-        cudaStream_t cs = copyStream;
-        std::int32_t* stage[2] = {pinned[0], pinned[1]};
-        // pinned staging: async device->host pieces, host memcpy of the previous
-        // piece meanwhile (pageable destinations would serialise the driver)
-        auto drain = [dst, src, cur, dev, cs, stage] {
-            cudaSetDevice(dev);
-            const std::size_t total = static_cast<std::size_t>(cur), piece = kPinnedInts;
-            std::size_t prevOff = 0, prevLen = 0;
-            int k = 0;
-            for (std::size_t off = 0; off < total || prevLen; off += piece, k ^= 1) {
-                const std::size_t len = off < total ? std::min(piece, total - off) : 0;
-                if (len)
-                    cudaMemcpyAsync(stage[k], src + off, len * 4, cudaMemcpyDeviceToHost, cs);
-                if (prevLen) parallel_copy(dst + prevOff, stage[k ^ 1], prevLen * 4);
-                cudaStreamSynchronize(cs);
-                prevOff = off;
-                prevLen = len;
+        }
+        if (!pooled) {
+            auto chunk = host_events(total);
+            segs.emplace_back(chunk.get(), total);
+            chunks->emplace_back(std::move(chunk), total);
+        }
+        cudaMemcpyAsync(rowD, rowOff.data(), rowOff.size() * 8, cudaMemcpyHostToDevice, cs);
+        std::vector<long long> rel(cnt.size());
+        std::size_t out = 0;  // events written to the destination so far
+        for (std::size_t c = 0; c + 1 < cuts.size(); ++c) {
+            const std::int64_t a = cuts[c], b = cuts[c + 1];
+            if (a == b) continue;
+            const long long base = evOff[a * nP];
+            const std::size_t n = static_cast<std::size_t>(evOff[b * nP] - base);
+            for (std::int64_t i = a * nP; i < b * nP; ++i) rel[i] = evOff[i] - base;
+            cudaMemcpyAsync(evD + a * nP, rel.data() + a * nP, (b - a) * nP * 8,
+                            cudaMemcpyHostToDevice, cs);
+            ssbk::raster_decode_kernel<<<static_cast<unsigned>((b - a) * nP), 256, 0, cs>>>(
+                arena, rowD + a, evD + a * nP, R, countsDev + a * nP, ev);
+            // device stage -> destination segments
+            std::size_t done = 0;
+            while (done < n) {
+                std::size_t o = out + done, si = 0;
+                while (o >= segs[si].second) o -= segs[si++].second;
+                const std::size_t len = std::min(n - done, segs[si].second - o);
+                if (pooled) {
+                    cudaMemcpyAsync(segs[si].first + o, ev + done, len * 4, cudaMemcpyDeviceToHost, cs);
+                } else {
+                    // pinned staging, host copy of the previous piece meanwhile
+                    std::size_t prevOff = 0, prevLen = 0;
+                    int k = 0;
+                    for (std::size_t p0 = 0; p0 < len || prevLen; p0 += kPinnedInts, k ^= 1) {
+                        const std::size_t l = p0 < len ? std::min(kPinnedInts, len - p0) : 0;
+                        if (l)
+                            cudaMemcpyAsync(stage[k], ev + done + p0, l * 4, cudaMemcpyDeviceToHost, cs);
+                        if (prevLen) parallel_copy(segs[si].first + o + prevOff, stage[k ^ 1], prevLen * 4);
+                        cudaStreamSynchronize(cs);
+                        prevOff = p0;
+                        prevLen = l;
+                    }
+                }
+                done += len;
             }
-        };
-        if (wait) drain();
-        else copier = std::thread(drain);
-    }
-    const long long zero = 0;
-    CK(cudaMemcpy(raster.cursor + parity, &zero, sizeof(long long), cudaMemcpyHostToDevice));
-    knownCursor = 0;
-    knownWin = epochStart = launchesDone;
+            cudaStreamSynchronize(cs);  // the stage is reused by the next chunk
+            out += n;
+        }
+    };
+    if (wait) drain();
+    else copier = std::thread(drain);
 }
 
-// Raster bookkeeping before a launch of M windows: learns the cursor of the
-// launch kRing back and flushes the arena if the worst case may overflow it.
-// Returns the launch's worst-case event count.
+// Raster bookkeeping before a launch of M windows of W steps: flush the
+// arena if they would not fit (their size is fixed).  Returns their words.
 std::int64_t DeviceEngine::Impl::pre_launch(int W, int M) {
-    const std::int64_t add = static_cast<std::int64_t>(W) * M * totalNeurons;
-    if (launchesDone - kRing >= std::max(epochStart, knownWin)) {
-        const std::int64_t idx = launchesDone - kRing;
-        CK(cudaEventSynchronize(ringEv[idx % kRing]));
-        knownCursor = ringVal[idx % kRing];
-        knownWin = idx + 1;
-    }
-    std::int64_t bound = knownCursor + add;
-    for (std::int64_t l = knownWin; l < launchesDone; ++l) bound += ringAdd[l % kRing];
-    if (bound > rasterCap) flush_raster();
+    const std::int64_t add = static_cast<std::int64_t>(W) * M * raster.rowWords;
+    if (cursorHost + add > rasterCap) flush_raster();
     return add;
 }
 
 void DeviceEngine::Impl::post_launch(int W, int M, std::int64_t add) {
     windowsLaunched += M;
     stepsDone += static_cast<std::int64_t>(W) * M;
-    const int slot = static_cast<int>(launchesDone % kRing);
-    CK(cudaMemcpyAsync(ringVal + slot, raster.cursor + (windowsLaunched & 1), sizeof(long long),
-                       cudaMemcpyDeviceToHost, stream));
-    CK(cudaEventRecord(ringEv[slot], stream));
-    ringAdd[slot] = add;
+    cursorHost += add;
+    for (int i = 0; i < M; ++i) arenaWins.push_back(W);
     ++launchesDone;
 }
 
@@ -1927,9 +2013,8 @@ void DeviceEngine::Impl::release() {
     eventPool.clear();
     for (cudaEvent_t e : capEvents) cudaEventDestroy(e);
     capEvents.clear();
-    for (cudaEvent_t& e : ringEv)
-        if (e) cudaEventDestroy(e), e = nullptr;
-    if (ringVal) cudaFreeHost(ringVal), ringVal = nullptr;
+    if (flushEv) cudaEventDestroy(flushEv), flushEv = nullptr;
+    if (pinnedConst) cudaFreeHost(pinnedConst), pinnedConst = nullptr;
     for (void* p : allocations) cudaFree(p);
     allocations.clear();
     for (cudaStream_t s : auxStreams) cudaStreamDestroy(s);
