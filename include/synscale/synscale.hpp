@@ -284,7 +284,12 @@ NetworkSpec build_mbody_net(std::int32_t nPN, std::int32_t nLHI, std::int32_t nK
 
 // ---- engine (reference engine.hpp:14-104) ----------------------------------
 
-enum class StorageMode { FromSpec, ForceDense, ForceSparse };
+// Auto (B200 extension): each group takes dense storage when its connection
+// density outDegree / nPost is at least auto_dense_threshold() (measured
+// crossover of the device kernels), CRS below it.  Like the
+// reference's modes it never changes results (engine.hpp:15-18).
+enum class StorageMode { FromSpec, ForceDense, ForceSparse, Auto };
+double auto_dense_threshold();
 
 struct SpikeEvent {
     std::int64_t step;

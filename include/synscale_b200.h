@@ -59,7 +59,8 @@ enum { SSB_STORAGE_DENSE = 0, SSB_STORAGE_SPARSE = 1 };
  * the rule is stated in DESIGN.md §1 (row A22). */
 enum { SSB_PLASTICITY_NONE = 0, SSB_PLASTICITY_STDP = 1 };
 /* StorageMode (engine.hpp:18) */
-enum { SSB_MODE_FROM_SPEC = 0, SSB_MODE_FORCE_DENSE = 1, SSB_MODE_FORCE_SPARSE = 2 };
+enum { SSB_MODE_FROM_SPEC = 0, SSB_MODE_FORCE_DENSE = 1, SSB_MODE_FORCE_SPARSE = 2,
+       SSB_MODE_AUTO = 3 /* extension: dense iff outDegree / nPost >= ssb_auto_dense_threshold() */ };
 /* WeightDist::Kind (matrix.hpp:15-16) */
 enum { SSB_WEIGHT_CONSTANT = 0, SSB_WEIGHT_UNIFORM = 1 };
 /* PopulationState fields (engine.hpp:48-54) */
@@ -216,6 +217,8 @@ typedef struct ssb_sim ssb_sim;
 
 /* ---- library ------------------------------------------------------------ */
 SSB_API const char* ssb_version(void);
+/* StorageMode Auto's density threshold (extension; env SSB_AUTO_DENSITY). */
+SSB_API double ssb_auto_dense_threshold(void);
 SSB_API int ssb_device_count(void);
 
 /* ---- spec helpers (network.cpp) ------------------------------------------- */

@@ -17,7 +17,7 @@ SSB_OK, SSB_ERR_INTERNAL, SSB_ERR_SPEC = 0, 1, 2
 MODEL_IZHIKEVICH, MODEL_POISSON, MODEL_CONDLIF, MODEL_TRAUBMILES = 0, 1, 2, 3
 SIGN_EXC, SIGN_INH = 0, 1
 STORAGE_DENSE, STORAGE_SPARSE = 0, 1
-MODE_FROM_SPEC, MODE_FORCE_DENSE, MODE_FORCE_SPARSE = 0, 1, 2
+MODE_FROM_SPEC, MODE_FORCE_DENSE, MODE_FORCE_SPARSE, MODE_AUTO = 0, 1, 2, 3
 WEIGHT_CONSTANT, WEIGHT_UNIFORM = 0, 1
 (FIELD_V, FIELD_U, FIELD_GEXC, FIELD_GINH, FIELD_EXCIN, FIELD_INHIN, FIELD_NANFLAG,
  FIELD_FLAGGED, FIELD_M, FIELD_H, FIELD_N) = range(11)
@@ -122,6 +122,7 @@ _vp, _cp, _sz = C.c_void_p, C.c_char_p, C.c_size_t
 # name: (restype, argtypes)
 _SIGNATURES = {
     "ssb_version": (_cp, []),
+    "ssb_auto_dense_threshold": (C.c_double, []),
     "ssb_device_count": (C.c_int, []),
     "ssb_validate": (C.c_int, [P(ssb_net_desc), _cp, _sz]),
     "ssb_build_mbody": (C.c_int, [_i32, _i32, _i32, _i32, P(_dbl), _u64, P(ssb_mbody_opts),

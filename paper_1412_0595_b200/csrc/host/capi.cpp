@@ -298,6 +298,7 @@ StorageMode to_mode(int m) {
     case SSB_MODE_FROM_SPEC: return StorageMode::FromSpec;
     case SSB_MODE_FORCE_DENSE: return StorageMode::ForceDense;
     case SSB_MODE_FORCE_SPARSE: return StorageMode::ForceSparse;
+    case SSB_MODE_AUTO: return StorageMode::Auto;
     }
     throw SpecError("unknown storage mode " + std::to_string(m));
 }
@@ -347,7 +348,9 @@ void to_c(const OccupancyResult& r, ssb_occupancy_result* o) {
 
 extern "C" {
 
-const char* ssb_version(void) { return "synscale-b200 0.1 (sm_100a)"; }
+const char* ssb_version(void) { return "synscale-b200 0.2 (sm_100a)"; }
+
+double ssb_auto_dense_threshold(void) { return synscale::auto_dense_threshold(); }
 
 int ssb_device_count(void) { return ssb::device_count(); }
 

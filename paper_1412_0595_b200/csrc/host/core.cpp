@@ -1,6 +1,7 @@
 // core.cpp — spec -> device network compile (reference Simulation ctor,
 // engine.cpp:146-245), stepping contract (engine.cpp:316-319, 385-401) and
 // result collection.
+#include <cstdlib>
 #include "core.hpp"
 
 #include <atomic>
@@ -29,6 +30,23 @@ double spike_rate(std::int64_t count, std::int32_t size, double durationMs) {
 
 }  // namespace
 
+}  // namespace ssb
+
+namespace synscale {
+// The density at and above which StorageMode::Auto stores a group dense: the
+// crossover of the window kernels on B200 (profiles/r02_sweeps.md); the
+// environment variable SSB_AUTO_DENSITY overrides it.
+double auto_dense_threshold() {
+    static const double t = [] {
+        const char* e = std::getenv("SSB_AUTO_DENSITY");
+        return e ? std::atof(e) : 0.25;
+    }();
+    return t;
+}
+}  // namespace synscale
+
+namespace ssb {
+
 void build_group_matrix(const NetworkSpec& spec, StorageMode mode, int gi,
                         std::optional<DenseMatrix>& dense, std::optional<CrsMatrix>& sparse) {
     const auto& gs = spec.synapses.at(gi);
@@ -37,9 +55,13 @@ void build_group_matrix(const NetworkSpec& spec, StorageMode mode, int gi,
     if (!pre || !post) throw SpecError("group '" + gs.name + "' names an unknown population");
     const std::int32_t nPre = group_pre_count(gs, pre->size), nPost = post->size;
     const bool inhibitory = gs.sign == SynapseSign::Inhibitory;
-    const StorageKind eff = mode == StorageMode::ForceDense    ? StorageKind::Dense
-                            : mode == StorageMode::ForceSparse ? StorageKind::Sparse
-                                                               : gs.storage;
+    const StorageKind eff =
+        mode == StorageMode::ForceDense    ? StorageKind::Dense
+        : mode == StorageMode::ForceSparse ? StorageKind::Sparse
+        : mode == StorageMode::Auto
+            ? (static_cast<double>(gs.outDegree) >= auto_dense_threshold() * nPost ? StorageKind::Dense
+                                                                                   : StorageKind::Sparse)
+            : gs.storage;
     detail::OutdegreeRows rows;
     rows.begin(nPre, nPost, gs.outDegree, gs.baseWeight, inhibitory ? -1 : +1,
                derive_seed(spec.globalSeed, gs.name));  // engine.cpp:223

@@ -176,6 +176,7 @@ std::string run_summary_to_json(const NetworkSpec& spec, const RunResult& result
     o << "  \"storage\": "
       << (mode == StorageMode::ForceDense    ? "\"dense\""
           : mode == StorageMode::ForceSparse ? "\"sparse\""
+          : mode == StorageMode::Auto        ? "\"auto\""
                                              : "\"spec\"")
       << ",\n";
     o << "  \"sumNaNs\": " << result.sumNaNs << ",\n";

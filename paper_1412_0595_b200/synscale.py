@@ -82,6 +82,7 @@ class StorageMode(enum.IntEnum):
     FromSpec = L.MODE_FROM_SPEC
     ForceDense = L.MODE_FORCE_DENSE
     ForceSparse = L.MODE_FORCE_SPARSE
+    Auto = L.MODE_AUTO  # extension: dense iff outDegree / nPost >= auto_dense_threshold()
 
 
 @dataclass
@@ -1033,6 +1034,11 @@ def device_preset(name: str) -> DeviceSpec:
     err = _err()
     _raise(lib.ssb_device_preset(name.encode(), C.byref(d), err, len(err)), err.value.decode())
     return DeviceSpec.from_c(d)
+
+
+def auto_dense_threshold() -> float:
+    """StorageMode.Auto's density threshold (extension; env SSB_AUTO_DENSITY)."""
+    return float(lib.ssb_auto_dense_threshold())
 
 
 def device_preset_names() -> List[str]:

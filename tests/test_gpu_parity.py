@@ -623,3 +623,20 @@ def test_bench_split_networks_match_parity_golden(world):
     assert counts == gold["counts"]
     assert specs.raster_checksum(r.raster.step, r.raster.population, r.raster.neuron) == \
         int(gold["checksum"])
+
+
+@pytest.mark.parametrize("frac", [0.001, 0.05, 0.3, 0.5])
+def test_storage_mode_auto_matches_reference_modes(oracle_mod, frac):
+    """StorageMode.Auto never changes results (reference engine.hpp:15-18): at
+    densities on both sides of the threshold the raster and state equal the
+    oracle's FromSpec run bit for bit, and the chosen layout follows density."""
+    spec = specs.mbody_spec(20_000, frac, 40.0)
+    g = gpu_sim(spec, S.StorageMode.Auto, window=64)
+    o = cpu_sim(oracle_mod, spec, S.StorageMode.FromSpec)
+    rg = g.finish()
+    ro = o.finish()
+    assert np.array_equal(rg.raster.step, ro[0]) and np.array_equal(rg.raster.neuron, ro[2])
+    assert np.array_equal(rg.raster.population, ro[1])
+    assert_state_equal(g, o, spec, f"auto {frac}")
+    dense_pn_kc = g.group_dense("pn_kc") is not None
+    assert dense_pn_kc == (frac >= S.auto_dense_threshold())

@@ -285,3 +285,23 @@ def test_sweep_grid_validation_and_failure_rows():
     assert all(r.failed and r.sumNaNs == -1 and np.isnan(r.avgSpike) for r in rows)
     assert "13" in rows[0].error and "device" in rows[2].error.lower()
     assert seen == [(1, 4), (2, 4), (3, 4), (4, 4)]
+
+
+def test_storage_mode_auto_follows_density():
+    """StorageMode.Auto (extension): dense iff outDegree / nPost >= the threshold
+    (0.25 by default), the reference's own storage flag otherwise ignored."""
+    t = S.auto_dense_threshold()
+    assert 0.0 < t <= 1.0
+    for frac in (0.001, 0.05, 0.2, 0.25, 0.5, 1.0):
+        spec = specs.mbody_spec(4000, frac, 5.0)
+        for g in spec.synapses:
+            post = spec.populations[spec.pop_index(g.post)]
+            kind, m = S.build_group(spec, g.name, S.StorageMode.Auto)
+            assert kind == ("dense" if g.outDegree >= t * post.size else "sparse"), (frac, g.name)
+            # same matrix as the explicit modes
+            ref = S.build_group(spec, g.name, S.StorageMode.ForceDense if kind == "dense"
+                                else S.StorageMode.ForceSparse)[1]
+            if kind == "dense":
+                assert np.array_equal(m, ref)
+            else:
+                assert all(np.array_equal(a, b) for a, b in zip(m, ref))
