@@ -316,6 +316,21 @@ SSB_API int ssb_propagate_crs_dev(const float* g, const int32_t* post_ind,
                                   const int32_t* seg, int32_t tile, int32_t n_pre, int32_t n_post,
                                   const int32_t* spikes, int32_t n_spikes, float* acc,
                                   void* stream);
+/* Column-sliced CRS (extension): the matrix re-laid as slices of 32 post
+ * columns (entry k of column 32 s + l at slice_off[s] + 32 k + l: its pre row,
+ * -1 for padding, and value; rows ascending within a column).  With rows /
+ * vals NULL only *needed (entries incl. padding) and slice_off
+ * [ceil(n_post / 32) + 1] are written.  Host arrays. */
+SSB_API int ssb_crs_slices(const float* g, const int32_t* post_ind, const int64_t* row_start,
+                           int32_t n_pre, int32_t n_post, int64_t* slice_off, int32_t* rows,
+                           float* vals, int64_t cap, int64_t* needed, char* err, size_t errlen);
+/* propagate(CrsMatrix) over column slices (device pointers): bit-identical to
+ * the reference for a spike list in ascending order without repeats (the
+ * engine's lists); coalesced loads at every density. */
+SSB_API int ssb_propagate_crs_sliced_dev(const int32_t* rows, const float* vals,
+                                         const int64_t* slice_off, int32_t n_pre, int32_t n_post,
+                                         const int32_t* spikes, int32_t n_spikes, float* acc,
+                                         void* stream);
 /* detect_nans (engine.cpp:27-51) on host arrays; runs on the GPU. Pointers a
  * model does not use may be NULL. Returns newly flagged via *newly. */
 SSB_API int ssb_detect_nans(int32_t model, const float* v, const float* u, const float* g_exc,

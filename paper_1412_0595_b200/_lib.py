@@ -156,6 +156,9 @@ _SIGNATURES = {
     "ssb_propagate_dense_dev": (C.c_int, [_vp, _i32, _i32, _vp, _i32, _vp, _vp]),
     "ssb_crs_segments_dev": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _vp]),
     "ssb_propagate_crs_dev": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
+    "ssb_crs_slices": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _i64, _vp, C.c_char_p,
+                                 C.c_size_t]),
+    "ssb_propagate_crs_sliced_dev": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _vp]),
     "ssb_detect_nans": (C.c_int, [_i32, P(_f32), P(_f32), P(_f32), P(_f32), P(_u8), _i64, P(_i64),
                                   P(_i64), _cp, _sz]),
     "ssb_create": (C.c_int, [P(ssb_net_desc), _i32, P(ssb_engine_opts), P(_vp), _cp, _sz]),

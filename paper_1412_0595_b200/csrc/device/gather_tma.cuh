@@ -323,3 +323,58 @@ __global__ void __launch_bounds__(kRsThreads) dense_window_rowstream_kernel(
     }
     if (t == 0) trace_block(0xfffffffcull, tStart);
 }
+
+// ---- CRS propagate over column slices (reference propagate(Crs),
+//      engine.cpp:69-80) --------------------------------------------------------
+// The matrix re-laid once (host, ssb_crs_slices) as slices of 32 post columns:
+// slice s holds, for k = 0 .. len_s - 1 and lane l, the k-th entry of column
+// 32 s + l (its pre row and value; row -1 pads a shorter column), rows
+// ascending within a column.  Lane l folds column 32 s + l over its entries
+// whose row is spiking (a bitmask in shared memory), so every load of the
+// kernel is a coalesced 128-byte line and every column's adds arrive in
+// ascending row order: bit-identical to the reference's row-by-row scatter
+// for a spike list in ascending order without repeats (the engine's lists).
+__global__ void __launch_bounds__(256) propagate_crs_sliced_kernel(
+    const int* __restrict__ rows, const float* __restrict__ vals,
+    const long long* __restrict__ sliceOff, int nPre, int nPost, const int* __restrict__ spikes,
+    int nSpikes, float* __restrict__ acc) {
+    extern __shared__ uint32_t s_spk[];  // [(nPre + 31) / 32]
+    const int nw = (nPre + 31) >> 5;
+    for (int i = threadIdx.x; i < nw; i += blockDim.x) s_spk[i] = 0u;
+    __syncthreads();
+    for (int k = threadIdx.x; k < nSpikes; k += blockDim.x) {
+        const int r = spikes[k];
+        if ((unsigned)r < (unsigned)nPre) atomicOr(&s_spk[r >> 5], 1u << (r & 31));
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int nSlices = (nPost + 31) >> 5;
+    for (int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nSlices;
+         s += gridDim.x * (blockDim.x >> 5)) {
+        const int j = s * 32 + lane;
+        const long long base = sliceOff[s];
+        const int len = static_cast<int>((sliceOff[s + 1] - base) >> 5);
+        const int* __restrict__ R = rows + base + lane;
+        const float* __restrict__ V = vals + base + lane;
+        float a = j < nPost ? acc[j] : 0.f;
+        int k = 0;
+        constexpr int U = 16;  // loads in flight per lane (DRAM latency x bandwidth)
+        for (; k + U <= len; k += U) {
+            int r[U];
+            float v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                r[u] = __ldg(R + (k + u) * 32);
+                v[u] = __ldg(V + (k + u) * 32);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (r[u] >= 0 && ((s_spk[r[u] >> 5] >> (r[u] & 31)) & 1u)) a = __fadd_rn(a, v[u]);
+        }
+        for (; k < len; ++k) {
+            const int r = __ldg(R + k * 32);
+            if (r >= 0 && ((s_spk[r >> 5] >> (r & 31)) & 1u)) a = __fadd_rn(a, __ldg(V + k * 32));
+        }
+        if (j < nPost) acc[j] = a;
+    }
+}

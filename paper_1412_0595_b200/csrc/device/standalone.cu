@@ -10,6 +10,7 @@
 
 #include "../engine.hpp"
 #include "kernels.cuh"
+#include "synscale/synscale.hpp"
 
 namespace ssb {
 
@@ -77,6 +78,53 @@ void device_propagate_crs_dev(const float* g, const std::int32_t* ind, const std
     CK(cudaGetLastError());
 }
 
+std::int64_t crs_slices(const float* g, const std::int32_t* ind, const std::int64_t* rowStart,
+                        int nPre, int nPost, std::int64_t* sliceOff, std::int32_t* rows,
+                        float* vals, std::int64_t cap) {
+    const int nSlices = (nPost + 31) / 32;
+    std::vector<std::int64_t> colLen(static_cast<std::size_t>(nPost), 0);
+    for (std::int64_t k = 0; k < rowStart[nPre]; ++k) {
+        if (ind[k] < 0 || ind[k] >= nPost) throw synscale::SpecError("post index out of range");
+        ++colLen[ind[k]];
+    }
+    sliceOff[0] = 0;
+    for (int s = 0; s < nSlices; ++s) {
+        std::int64_t m = 0;
+        for (int l = 0; l < 32 && s * 32 + l < nPost; ++l) m = std::max(m, colLen[s * 32 + l]);
+        sliceOff[s + 1] = sliceOff[s] + 32 * m;
+    }
+    const std::int64_t need = sliceOff[nSlices];
+    if (!rows || !vals) return need;
+    if (cap < need) throw synscale::SpecError("slice arrays too small");
+    std::fill(rows, rows + need, -1);
+    std::fill(vals, vals + need, 0.0f);
+    std::vector<std::int64_t> fill(static_cast<std::size_t>(nPost), 0);
+    for (int r = 0; r < nPre; ++r)  // rows ascending: every column stays sorted
+        for (std::int64_t k = rowStart[r]; k < rowStart[r + 1]; ++k) {
+            const int j = ind[k];
+            const std::int64_t at = sliceOff[j / 32] + 32 * fill[j]++ + (j % 32);
+            rows[at] = r;
+            vals[at] = g[k];
+        }
+    return need;
+}
+
+void device_propagate_crs_sliced_dev(const std::int32_t* rows, const float* vals,
+                                     const std::int64_t* sliceOff, int nPre, int nPost,
+                                     const std::int32_t* spikes, int nSpikes, float* acc,
+                                     void* stream) {
+    if (nPost <= 0 || nSpikes <= 0) return;
+    const int smem = ((nPre + 31) / 32) * 4;
+    if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(ssbk::propagate_crs_sliced_kernel,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int slices = (nPost + 31) / 32;
+    const int blocks = std::min((slices + 7) / 8, 148 * 8);
+    ssbk::propagate_crs_sliced_kernel<<<blocks, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+        rows, vals, reinterpret_cast<const long long*>(sliceOff), nPre, nPost, spikes, nSpikes, acc);
+    CK(cudaGetLastError());
+}
+
 void device_propagate_dense(const float* w, int nPre, int nPost, const std::int32_t* spikes,
                             std::int64_t nSpikes, float* acc) {
     require_device();
@@ -95,6 +143,31 @@ void device_propagate_crs(const float* g, const std::int32_t* ind, const std::in
                           float* acc) {
     require_device();
     const std::size_t nnz = static_cast<std::size_t>(rowStart[nPre]);
+    bool ascending = true;
+    for (std::int64_t k = 1; k < nSpikes && ascending; ++k) ascending = spikes[k] > spikes[k - 1];
+    if (ascending && nSpikes > 0 && nPost > 0) {
+        // column slices: coalesced at every density (gather_tma.cuh)
+        std::vector<std::int64_t> off(static_cast<std::size_t>((nPost + 31) / 32) + 1);
+        const std::int64_t need = crs_slices(g, ind, rowStart, nPre, nPost, off.data(), nullptr,
+                                             nullptr, 0);
+        std::vector<std::int32_t> rows(static_cast<std::size_t>(need));
+        std::vector<float> vals(static_cast<std::size_t>(need));
+        crs_slices(g, ind, rowStart, nPre, nPost, off.data(), rows.data(), vals.data(), need);
+        Buf dR(rows.size() * 4), dV(vals.size() * 4), dO(off.size() * 8),
+            dS(static_cast<std::size_t>(nSpikes) * 4), dA(static_cast<std::size_t>(nPost) * 4);
+        if (need) {
+            CK(cudaMemcpy(dR.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dV.p, vals.data(), vals.size() * 4, cudaMemcpyHostToDevice));
+        }
+        CK(cudaMemcpy(dO.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dS.p, spikes, static_cast<std::size_t>(nSpikes) * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dA.p, acc, static_cast<std::size_t>(nPost) * 4, cudaMemcpyHostToDevice));
+        device_propagate_crs_sliced_dev(dR.as<std::int32_t>(), dV.as<float>(), dO.as<std::int64_t>(),
+                                        nPre, nPost, dS.as<std::int32_t>(),
+                                        static_cast<int>(nSpikes), dA.as<float>(), nullptr);
+        CK(cudaMemcpy(acc, dA.p, static_cast<std::size_t>(nPost) * 4, cudaMemcpyDeviceToHost));
+        return;
+    }
     const int nTiles = (nPost + kTile - 1) / kTile;
     Buf dG(nnz * 4), dI(nnz * 4), dR((static_cast<std::size_t>(nPre) + 1) * 8),
         dSeg(static_cast<std::size_t>(nPre) * (nTiles + 1) * 4),

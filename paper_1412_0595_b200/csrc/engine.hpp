@@ -213,6 +213,15 @@ void device_propagate_dense_dev(const float* w, int nPre, int nPost, const std::
                                 int nSpikes, float* acc, void* stream);
 void device_crs_segments_dev(const std::int32_t* ind, const std::int64_t* rowStart, int nPre,
                              int nPost, int tile, std::int32_t* seg, void* stream);
+// Column slices of a CRS matrix (ssb_crs_slices); returns the entries incl.
+// padding (rows / vals may be null: sizes only).  Throws SpecError.
+std::int64_t crs_slices(const float* g, const std::int32_t* ind, const std::int64_t* rowStart,
+                        int nPre, int nPost, std::int64_t* sliceOff, std::int32_t* rows,
+                        float* vals, std::int64_t cap);
+void device_propagate_crs_sliced_dev(const std::int32_t* rows, const float* vals,
+                                     const std::int64_t* sliceOff, int nPre, int nPost,
+                                     const std::int32_t* spikes, int nSpikes, float* acc,
+                                     void* stream);
 void device_propagate_crs_dev(const float* g, const std::int32_t* ind, const std::int32_t* seg,
                               int tile, int nPre, int nPost, const std::int32_t* spikes,
                               int nSpikes, float* acc, void* stream);

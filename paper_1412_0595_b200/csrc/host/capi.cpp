@@ -2,7 +2,9 @@
 // descriptors to the C++ model, runs everything behind try/catch and maps
 // SpecError -> SSB_ERR_SPEC, anything else -> SSB_ERR_INTERNAL.
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
+#include <vector>
 #include <string>
 
 #include "../../../include/synscale_b200.h"
@@ -710,6 +712,25 @@ int ssb_propagate_crs_dev(const float* g, const int32_t* post_ind, const int32_t
         if (tile < 32 || tile > 1024 || tile % 32) throw SpecError("tile must be a warp multiple <= 1024");
         ssb::device_propagate_crs_dev(g, post_ind, seg, tile, n_pre, n_post, spikes, n_spikes, acc,
                                       stream);
+    });
+}
+
+int ssb_crs_slices(const float* g, const int32_t* post_ind, const int64_t* row_start,
+                   int32_t n_pre, int32_t n_post, int64_t* slice_off, int32_t* rows, float* vals,
+                   int64_t cap, int64_t* needed, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (n_pre < 0 || n_post < 0 || !row_start || !slice_off || !needed)
+            throw SpecError("bad CRS slice arguments");
+        *needed = ssb::crs_slices(g, post_ind, row_start, n_pre, n_post, slice_off, rows, vals, cap);
+    });
+}
+
+int ssb_propagate_crs_sliced_dev(const int32_t* rows, const float* vals, const int64_t* slice_off,
+                                 int32_t n_pre, int32_t n_post, const int32_t* spikes,
+                                 int32_t n_spikes, float* acc, void* stream) {
+    return guarded(nullptr, 0, [&] {
+        ssb::device_propagate_crs_sliced_dev(rows, vals, slice_off, n_pre, n_post, spikes, n_spikes,
+                                             acc, stream);
     });
 }
 

@@ -107,7 +107,7 @@ def main():
             f.write(launch_table(per, a.launches_title or f"ncu launch list ({a.launches})"))
     if a.kc_metrics:
         per = launches(a.kc_metrics)
-        kc = [d for d in per.values() if d["name"].startswith("condlif_window")
+        kc = [d for d in per.values() if d["name"].startswith("condlif_")
               and int(d["grid"].strip("()").split(",")[0]) > 1]
         inst = sorted(d["sm__inst_executed.sum"] for d in kc)
         med = inst[len(inst) // 2]
@@ -116,7 +116,7 @@ def main():
         us = sorted(d.get("gpu__time_duration.sum", 0.0) for d in kc)
         clk = [d.get("sm__cycles_elapsed.avg.per_second", 0.0) for d in kc]
         out = {"round": a.round, "source": a.kc_source or os.path.basename(a.kc_metrics),
-               "kernel": "condlif_window_kernel (KC update, multi-block)", "launches": len(kc),
+               "kernel": f"{kc[0]['name']} (KC update, multi-block)", "launches": len(kc),
                "neurons": a.kc_neurons, "steps_per_launch": a.kc_steps,
                "warp_inst_per_launch_median": med,
                "warp_inst_per_neuron_step": med / (a.kc_neurons * a.kc_steps),

@@ -78,6 +78,24 @@ def density():
                                  seg.data_ptr(), sp)
         acc_d = torch.zeros(n_post, dtype=torch.float32, device="cuda")
         acc_s = torch.zeros(n_post, dtype=torch.float32, device="cuda")
+        acc_c = torch.zeros(n_post, dtype=torch.float32, device="cuda")
+        # column-sliced layout (ssb_crs_slices, host), then device copies
+        import ctypes as C
+        n_sl = (n_post + 31) // 32
+        off = np.zeros(n_sl + 1, np.int64)
+        need = C.c_int64()
+        err = C.create_string_buffer(256)
+        cols32 = np.ascontiguousarray(cols.astype(np.int32))
+        lib.ssb_crs_slices(vals.ctypes.data, cols32.ctypes.data, rs.ctypes.data, n_pre, n_post,
+                           off.ctypes.data, None, None, 0, C.byref(need), err, len(err))
+        srows = np.empty(need.value, np.int32)
+        svals = np.empty(need.value, np.float32)
+        lib.ssb_crs_slices(vals.ctypes.data, cols32.ctypes.data, rs.ctypes.data, n_pre, n_post,
+                           off.ctypes.data, srows.ctypes.data, svals.ctypes.data, need.value,
+                           C.byref(need), err, len(err))
+        d_sr = torch.from_numpy(srows).cuda()
+        d_sv = torch.from_numpy(svals).cuda()
+        d_so = torch.from_numpy(off).cuda()
 
         def dense():
             lib.ssb_propagate_dense_dev(dw.data_ptr(), n_pre, n_post, spikes.data_ptr(), n_pre,
@@ -87,17 +105,25 @@ def density():
             lib.ssb_propagate_crs_dev(dg.data_ptr(), di.data_ptr(), seg.data_ptr(), tile, n_pre,
                                       n_post, spikes.data_ptr(), n_pre, acc_s.data_ptr(), sp)
 
+        def sliced():
+            lib.ssb_propagate_crs_sliced_dev(d_sr.data_ptr(), d_sv.data_ptr(), d_so.data_ptr(),
+                                             n_pre, n_post, spikes.data_ptr(), n_pre,
+                                             acc_c.data_ptr(), sp)
+
         td, ts = timed(dense, acc_d.zero_), timed(sparse, acc_s.zero_)
+        tc = timed(sliced, acc_c.zero_)
         # parity: both kernels against the reference fold (rows ascending)
         ref = np.zeros(n_post, np.float32)
         for r in range(n_pre):
             ref += w[r]
         same = bool(np.array_equal(acc_d.cpu().numpy(), ref) and
-                    np.array_equal(acc_s.cpu().numpy(), ref))
+                    np.array_equal(acc_s.cpu().numpy(), ref) and
+                    np.array_equal(acc_c.cpu().numpy(), ref))
         nnz = int(len(vals))
         bd = n_pre * n_post * 4 + n_post * 8      # every weight once + acc read/write
         bs = nnz * 8 + n_pre * (n_tiles + 1) * 4 + n_post * 8
-        for kind, t, b in (("dense", td, bd), ("sparse", ts, bs)):
+        bc = int(need.value) * 8 + (n_sl + 1) * 8 + n_post * 8  # slices once + acc
+        for kind, t, b in (("dense", td, bd), ("sparse", ts, bs), ("sparse_sliced", tc, bc)):
             print(json.dumps({"sweep": "density_kernel", "frac": frac, "kernel": kind,
                               "nnz": nnz, "us": round(t * 1e6, 2),
                               "synaptic_events_per_s": nnz / t, "algorithmic_bytes": b,
@@ -111,9 +137,9 @@ def model(profile=False):
     from paper_1412_0595_b200 import synscale as S
     import torch
     n_kc, secs = 100_000, 0.2
-    for frac in (0.001, 0.01, 0.1, 0.5):
+    for frac in (0.001, 0.01, 0.05, 0.1, 0.25, 0.5):
         spec = specs.mbody_spec(n_kc, frac, secs * 1000.0 + 30.0)
-        for mode in (S.StorageMode.ForceSparse, S.StorageMode.ForceDense):
+        for mode in (S.StorageMode.ForceSparse, S.StorageMode.ForceDense, S.StorageMode.Auto):
             sim = S.Simulation(spec, mode, S.EngineOptions(window=256))
             sim.step(256)
             sim.sync()
@@ -129,7 +155,9 @@ def model(profile=False):
             d = sim.spike_counts() - c0
             idx = {p.name: i for i, p in enumerate(spec.populations)}
             ev = sum(int(d[idx[g.pre]]) * g.outDegree for g in spec.synapses)
+            layout = "dense" if sim.group_dense("pn_kc") is not None else "sparse"
             print(json.dumps({"sweep": "density_model", "frac": frac, "mode": mode.name,
+                              "pn_kc_layout": layout,
                               "us_per_step": round(t / steps * 1e6, 3),
                               "sim_wall": round(secs / t, 2), "synaptic_events_per_s": ev / t,
                               "kc_rate_hz": float(d[idx["kc"]]) / n_kc / secs}), flush=True)
