@@ -401,6 +401,8 @@ SSB_API int ssb_raster_drain_async(ssb_sim* sim);
 SSB_API void* ssb_stream(ssb_sim* sim); /* the handle's cudaStream_t */
 SSB_API int32_t ssb_window(const ssb_sim* sim); /* effective steps per launch window */
 SSB_API int32_t ssb_block_size(const ssb_sim* sim, int32_t pop);
+/* blocks of the population's update kernel (0: no update kernel) */
+SSB_API int32_t ssb_grid_size(const ssb_sim* sim, int32_t pop);
 SSB_API int32_t ssb_n_kernel_stats(const ssb_sim* sim);
 SSB_API int ssb_kernel_stats(ssb_sim* sim, ssb_kernel_stat* out, int32_t n);
 SSB_API int ssb_kernel_stats_reset(ssb_sim* sim);

@@ -189,6 +189,7 @@ _SIGNATURES = {
     "ssb_stream": (_vp, [_vp]),
     "ssb_window": (_i32, [_vp]),
     "ssb_block_size": (_i32, [_vp, _i32]),
+    "ssb_grid_size": (_i32, [_vp, _i32]),
     "ssb_n_kernel_stats": (_i32, [_vp]),
     "ssb_kernel_stats": (C.c_int, [_vp, P(ssb_kernel_stat), _i32]),
     "ssb_kernel_stats_reset": (C.c_int, [_vp]),

@@ -2290,6 +2290,7 @@ bool DeviceEngine::pull_weights(int group, float* dst, std::int64_t count) {
 void* DeviceEngine::stream() const { return impl_->stream; }
 int DeviceEngine::window() const { return impl_->Wmax; }
 int DeviceEngine::block_size(int pop) const { return impl_->pops.at(pop).block; }
+int DeviceEngine::grid_size(int pop) const { return impl_->pops.at(pop).grid; }
 bool DeviceEngine::step_mode() const { return impl_->stepMode; }
 std::int64_t DeviceEngine::device_bytes() const { return impl_->bytes; }
 std::int64_t DeviceEngine::kernel_launches() const { return impl_->kernelLaunches; }

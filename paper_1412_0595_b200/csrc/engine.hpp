@@ -184,6 +184,7 @@ public:
     void* stream() const;
     int window() const;
     int block_size(int pop) const;
+    int grid_size(int pop) const;
     bool step_mode() const;
     std::int64_t device_bytes() const;
     std::int64_t kernel_launches() const;  // kernels launched by step() so far

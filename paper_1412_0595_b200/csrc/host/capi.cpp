@@ -960,6 +960,11 @@ int32_t ssb_block_size(const ssb_sim* sim, int32_t pop) {
     return sim->core->engine().block_size(pop);
 }
 
+int32_t ssb_grid_size(const ssb_sim* sim, int32_t pop) {
+    if (!sim || pop < 0 || pop >= sim->core->n_pops()) return 0;
+    return sim->core->engine().grid_size(pop);
+}
+
 int32_t ssb_n_kernel_stats(const ssb_sim* sim) {
     return sim ? static_cast<int32_t>(const_cast<ssb_sim*>(sim)->core->engine().kernel_stats().size()) : 0;
 }

@@ -675,6 +675,11 @@ class Simulation:
         pi = pop if isinstance(pop, int) else self.spec.pop_index(pop)
         return int(lib.ssb_block_size(self._h, pi))
 
+    def grid_size(self, pop: Union[int, str]) -> int:
+        """Blocks of the population's update kernel."""
+        pi = pop if isinstance(pop, int) else self.spec.pop_index(pop)
+        return int(lib.ssb_grid_size(self._h, pi))
+
     def stream(self) -> int:
         return int(lib.ssb_stream(self._h) or 0)
 
