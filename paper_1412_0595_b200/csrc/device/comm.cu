@@ -24,6 +24,9 @@ struct Nccl {
     ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     const char* (*errorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
 };
 
 Nccl& nccl() {
@@ -41,6 +44,9 @@ Nccl& nccl() {
         n.allGather = reinterpret_cast<decltype(n.allGather)>(dlsym(n.lib, "ncclAllGather"));
         n.allReduce = reinterpret_cast<decltype(n.allReduce)>(dlsym(n.lib, "ncclAllReduce"));
         n.errorString = reinterpret_cast<decltype(n.errorString)>(dlsym(n.lib, "ncclGetErrorString"));
+        n.send = reinterpret_cast<decltype(n.send)>(dlsym(n.lib, "ncclSend"));
+        n.recv = reinterpret_cast<decltype(n.recv)>(dlsym(n.lib, "ncclRecv"));
+        n.commSplit = reinterpret_cast<decltype(n.commSplit)>(dlsym(n.lib, "ncclCommSplit"));
     });
     if (!n.lib || !n.getUniqueId || !n.commInitRank || !n.allGather || !n.allReduce)
         throw DeviceError("NCCL (libnccl.so.2) is not available for a multi-GPU run");
@@ -85,6 +91,27 @@ void Comm::allgather_u32(const void* send, void* recv, std::size_t count, cudaSt
 void Comm::allreduce_sum_u64(void* buf, std::size_t count, cudaStream_t s) {
     nck(nccl().allReduce(buf, buf, count, ncclUint64, ncclSum, static_cast<ncclComm_t>(comm_), s),
         "ncclAllReduce");
+}
+
+void Comm::send_f32(const void* buf, std::size_t count, int peer, cudaStream_t s) {
+    if (!nccl().send) throw DeviceError("ncclSend is not available");
+    nck(nccl().send(buf, count, ncclFloat32, peer, static_cast<ncclComm_t>(comm_), s), "ncclSend");
+}
+
+void Comm::recv_f32(void* buf, std::size_t count, int peer, cudaStream_t s) {
+    if (!nccl().recv) throw DeviceError("ncclRecv is not available");
+    nck(nccl().recv(buf, count, ncclFloat32, peer, static_cast<ncclComm_t>(comm_), s), "ncclRecv");
+}
+
+std::unique_ptr<Comm> Comm::split() const {
+    if (!nccl().commSplit) throw DeviceError("ncclCommSplit is not available");
+    ncclComm_t c = nullptr;
+    nck(nccl().commSplit(static_cast<ncclComm_t>(comm_), 0, rank_, &c, nullptr), "ncclCommSplit");
+    std::unique_ptr<Comm> out(new Comm());
+    out->comm_ = c;
+    out->world_ = world_;
+    out->rank_ = rank_;
+    return out;
 }
 
 }  // namespace ssb

@@ -279,6 +279,8 @@ struct DeviceEngine::Impl {
         int offBits = -1;           // shared copy of the window's spike bits (1-block pops)
         int tileN = 0;              // neurons per block
         int quad = 0;               // CondLif: neurons per thread of the quad kernel (0: tile kernel)
+        bool globalUse = false;     // some consumer group reads its global spikes (not row-split)
+        bool pipeSource = false;    // a row-split group reads its local lists
         int chunk = 1;              // steps per phase-A/phase-B chunk
         int offIn = 0;              // shared offset of the phase-A inputs
         std::vector<int> accGroups[2];  // group indices in spec order
@@ -307,6 +309,19 @@ struct DeviceEngine::Impl {
     bool serial = false;        // one stream, no graphs (profiling, virtual shards)
     bool ownsStream = true;
     std::unique_ptr<Comm> comm;  // NCCL, one process per GPU
+    // rank pipeline (ShardPlan::pipeSink): per row-split group, this rank's
+    // partial sums [Wmax + 1][nPost] per window-buffer set; chain and final
+    // hop on communicators of their own (split off comm)
+    struct PipeRt {
+        int gi = 0, post = 0, a = 0, nPost = 0;
+        std::string name;
+        float* buf[kMaxSets] = {};
+        ssbk::GroupDev dev[kMaxSets]{};
+    };
+    std::vector<PipeRt> pipes;
+    std::unique_ptr<Comm> chainComm, finalComm;
+    void enqueue_pipes(int pi, int W, int b, cudaStream_t sg, cudaStream_t sm);
+    void pipe_gather(const PipeRt& L, int W, int b, int first, cudaStream_t s);
     char* commScratch = nullptr;  // state gathers of split populations
     std::size_t commScratchBytes = 0;
     char* comm_scratch(std::size_t bytes) {
@@ -1135,6 +1150,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     for (const auto& g : net.groups) {
         auto& c = pops[g.pre].consumers;
         if (std::find(c.begin(), c.end(), g.post) == c.end()) c.push_back(g.post);
+        if (g.rowSplit) pops[g.pre].pipeSource = true;
+        else pops[g.pre].globalUse = true;
     }
 
     // groups
@@ -1220,7 +1237,24 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         meta.dense = g.dense;
         meta.preCount = g.preCount;
         meta.nPost = g.nPost;
+        meta.rowSplit = g.rowSplit;
         groupMeta.push_back(meta);
+        if (g.rowSplit) {  // rank pipeline: partial sums per window-buffer set
+            PipeRt L;
+            L.gi = static_cast<int>(gi);
+            L.post = g.post;
+            L.a = g.inhibitory ? 1 : 0;
+            L.nPost = g.nPost;
+            L.name = g.name;
+            for (int b = 0; b < nSets; ++b) {
+                L.buf[b] = alloc<float>(static_cast<std::size_t>(Wmax + 1) * g.nPost);
+                L.dev[b] = G;
+                L.dev[b].preList = pops[g.pre].kdev[b].list;  // this rank's own spikes,
+                L.dev[b].preCnt = pops[g.pre].kdev[b].count;  // local indices
+                L.dev[b].preN = pops[g.pre].n;
+            }
+            pipes.push_back(L);
+        }
     }
     for (auto& P : pops)
         for (int a = 0; a < 2; ++a)
@@ -1428,6 +1462,7 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
             for (int k = 0; k < A.ng; ++k) {
                 const auto& G = A.g[k];
                 const int gi = P.accGroups[a][k];
+                if (groupMeta[gi].rowSplit) continue;  // the rank pipeline fills it
                 float* out = A.buf + P.n;  // row w = 1
                 groups = true;
                 if (G.dense || G.fullRows) {
@@ -1505,7 +1540,7 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
         edge(sm, sp);
         launchStream = sp;
         // (split: the local raster's lists, or the counts the exchange carries)
-        if (P.grid > 1 && (!P.sharded || rasterLocal || P.rankCounts)) {
+        if (P.grid > 1 && (!P.sharded || rasterLocal || P.rankCounts || P.pipeSource)) {
             const int bs = std::min(1024, round_up((P.nwords + ssbk::kCompactK - 1) / ssbk::kCompactK, 32));
             launch("compact_window:" + P.name, [&] {
                 ssbk::compact_window_kernel<<<W, bs, 0, sp>>>(K.bits, P.nwords, P.n, K.list, K.count);
@@ -1516,7 +1551,7 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
     }
     // a split population's global spikes are needed by its consumers and a
     // global raster; a local raster of a sink population (DN) needs none
-    if (P.sharded && (!rasterLocal || !P.consumers.empty())) {
+    if (P.sharded && (!rasterLocal || P.globalUse)) {
         // the window's exchange: every rank's local bits, in rank order
         if (comm) {
             // collectives of one communicator must run in the same order on
@@ -1606,6 +1641,39 @@ void DeviceEngine::Impl::enqueue_tail(int W, int b, cudaStream_t s) {
     });
 }
 
+// Rank pipeline (ShardPlan::pipeSink): this rank's fold of a row-split group
+// over its own spiking pre rows, into its partial-sum buffer (first: from +0,
+// else continuing the partial sums already there).
+void DeviceEngine::Impl::pipe_gather(const PipeRt& L, int W, int b, int first, cudaStream_t s) {
+    launchStream = s;
+    launch_dense(L.dev[b], L.name, "pipe_gather:", L.buf[b] + L.nPost, L.nPost, 1, W, first, s);
+}
+
+// One window of the rank pipeline into population pi (real or emulated
+// world; virtual shards chain in lockstep): receive the previous rank's
+// partial sums, continue them over this rank's rows, pass them on; the last
+// rank hands the finished inputs to rank 0, which owns the population.
+void DeviceEngine::Impl::enqueue_pipes(int pi, int W, int b, cudaStream_t sg, cudaStream_t sm) {
+    const int R = world, rank = cfg.rank;
+    for (const auto& L : pipes) {
+        if (L.post != pi) continue;
+        const std::size_t cnt = static_cast<std::size_t>(W) * L.nPost;
+        float* rows = L.buf[b] + L.nPost;
+        if (chainComm && rank > 0) chainComm->recv_f32(rows, cnt, rank - 1, sg);
+        pipe_gather(L, W, b, rank == 0 ? 1 : 0, sg);
+        auto& P = pops[pi];
+        float* dst = P.accb[b][L.a].buf + P.n;
+        if (chainComm) {
+            if (rank < R - 1) chainComm->send_f32(rows, cnt, rank + 1, sg);
+            else finalComm->send_f32(rows, cnt, 0, sg);
+            if (rank == 0) finalComm->recv_f32(dst, cnt, R - 1, sm);
+        } else if (rank == 0 && P.n > 0) {  // emulated exchange (timing): own partials
+            CK(cudaMemcpyAsync(dst, rows, cnt * 4, cudaMemcpyDeviceToDevice, sg));
+            edge(sg, sm);
+        }
+    }
+}
+
 // M consecutive windows.  Each population's kernels run on its own stream;
 // cross-stream edges carry exactly the data dependencies: the pre
 // populations' spike lists of the same window, the reuse of a window-buffer
@@ -1665,6 +1733,7 @@ void DeviceEngine::Impl::enqueue_windows(int W, int M) {
                 }
                 if (stepMode && m >= 1) after(x, rdone[m - 1]);
             }
+            if (!pipes.empty() && !virtualShard) enqueue_pipes(pi, W, b, S(sg), S(sm));
             enqueue_pop(pi, W, b, S(sg), S(sm), S(sp));
             kdone[pi][m] = mark(sp);
         }
@@ -1897,7 +1966,11 @@ DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfgIn)
         if (g.plastic && split)
             throw synscale::SpecError("plastic group '" + g.name +
                                       "': learning runs on one GPU (split worlds are not supported)");
-    const ShardPlan plan = split ? plan_shards(net, R, cfg.shardMinSize, true) : ShardPlan{};
+    const bool pipeline = !(std::getenv("SSB_PIPELINE") && std::string(std::getenv("SSB_PIPELINE")) == "0");
+    const ShardPlan plan =
+        split ? plan_shards(net, R, cfg.shardMinSize, true,
+                            cfg.heavyPreThreshold > 0 ? cfg.heavyPreThreshold : 1024, pipeline)
+              : ShardPlan{};
     const int smCount = device_props(cfg.device).smCount;
     auto init = [&](Impl& m, int rank, cudaStream_t shared) {
         m.cfg = cfg;
@@ -1922,6 +1995,10 @@ DeviceEngine::DeviceEngine(const HostNet& net, const EngineConfig& cfgIn)
             const HostNet local = split ? shard_net(net, plan, rank, store) : HostNet{};
             if (split && !virt && !emulate) m.comm = std::make_unique<Comm>(R, rank, cfg.commId.data());
             m.build(split ? local : net);
+            if (m.comm && !m.pipes.empty()) {
+                m.chainComm = m.comm->split();
+                m.finalComm = m.comm->split();
+            }
         } catch (...) {
             m.release();
             throw;
@@ -1963,6 +2040,23 @@ void DeviceEngine::lockstep(int W) {
         m->lastWide = nullptr;
     }
     for (int pi : m0.order) {
+        // rank pipeline: shard r continues shard r-1's partial sums over its
+        // own rows; the last shard's are shard 0's (the owner's) inputs
+        for (std::size_t k = 0; k < m0.pipes.size(); ++k) {
+            if (m0.pipes[k].post != pi) continue;
+            const auto& L0 = m0.pipes[k];
+            const std::size_t cnt = static_cast<std::size_t>(W) * L0.nPost;
+            for (int r = 0; r < R; ++r) {
+                auto& L = all[r]->pipes[k];
+                if (r > 0)
+                    CK(cudaMemcpyAsync(L.buf[b] + L.nPost, all[r - 1]->pipes[k].buf[b] + L.nPost,
+                                       cnt * 4, cudaMemcpyDeviceToDevice, m0.stream));
+                all[r]->pipe_gather(L, W, b, r == 0 ? 1 : 0, m0.stream);
+            }
+            auto& P0 = m0.pops[pi];
+            CK(cudaMemcpyAsync(P0.accb[b][L0.a].buf + P0.n, all[R - 1]->pipes[k].buf[b] + L0.nPost,
+                               cnt * 4, cudaMemcpyDeviceToDevice, m0.stream));
+        }
         for (auto* m : all) m->enqueue_pop(pi, W, b, m0.stream);
         if (!m0.pops[pi].sharded) continue;
         const std::size_t words = m0.exchange_words(m0.pops[pi], W);

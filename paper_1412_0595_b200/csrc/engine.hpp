@@ -57,6 +57,11 @@ struct HostGroup {
     // extension F2: STDP (fp32 constants; trace decays float(exp(-dt/tau)))
     bool plastic = false;
     float aPlus = 0, aMinus = 0, decPlus = 0, decMinus = 0, wMax = 0;
+    // multi-GPU (ShardPlan::rowSplit): this rank holds the rows of its own
+    // pre-neuron range [preLo, preLo + nPre) and every post column; the fold
+    // continues rank by rank (DeviceEngine, rank pipeline)
+    bool rowSplit = false;
+    int preLo = 0;
 };
 
 struct HostNet {
@@ -100,11 +105,19 @@ struct ShardPlan {
     int world = 1;
     std::vector<std::vector<int>> bounds;
     std::vector<int> chunk;  // bounds[p][r] = min(r * chunk[p], n)
+    // rank pipeline: a sink population fed only by heavy dense groups from
+    // split populations is owned whole by rank 0 (chunk = n); each rank folds
+    // those groups over its own pre rows, continuing the previous rank's
+    // partial sums (ascending rows = the reference's order), the last rank
+    // hands the result to rank 0 -- no spike exchange for the pre population
+    std::vector<char> pipeSink;  // per population
+    std::vector<char> rowSplit;  // per group
     bool split(int p) const { return !bounds[p].empty(); }
 };
 // force: split even a world of one rank (a one-rank NCCL communicator runs
 // the whole exchange path; used to test it on one GPU)
-ShardPlan plan_shards(const HostNet& net, int world, int minSize, bool force = false);
+ShardPlan plan_shards(const HostNet& net, int world, int minSize, bool force = false,
+                      int heavyThreshold = 1024, bool pipeline = true);
 
 // Matrices owned by a rank's local network (column slices).
 struct ShardStore {

@@ -21,12 +21,15 @@ namespace {
 int round_up(int v, int u) { return (v + u - 1) / u * u; }
 }  // namespace
 
-ShardPlan plan_shards(const HostNet& net, int world, int minSize, bool force) {
+ShardPlan plan_shards(const HostNet& net, int world, int minSize, bool force, int heavyThreshold,
+                      bool pipeline) {
     ShardPlan plan;
     plan.world = std::max(1, world);
     const int np = static_cast<int>(net.pops.size());
     plan.bounds.assign(np, {});
     plan.chunk.assign(np, 0);
+    plan.pipeSink.assign(np, 0);
+    plan.rowSplit.assign(net.groups.size(), 0);
     if (plan.world == 1 && !force) return plan;
     // feed-forward check (the windowed schedule exchanges once per window)
     std::vector<std::vector<int>> succ(np);
@@ -59,6 +62,34 @@ ShardPlan plan_shards(const HostNet& net, int world, int minSize, bool force) {
         for (int r = 0; r <= R; ++r)
             b[r] = static_cast<int>(std::min<std::int64_t>(static_cast<std::int64_t>(r) * chunk, P.n));
     }
+    // rank pipeline (ShardPlan::pipeSink): a split sink whose every input is
+    // one heavy dense group per sign from a split pre population, whole pre
+    // range, at most kChainMaxPost (128) columns in 16-byte rows
+    if (R > 1 && pipeline) {
+        for (int p = 0; p < np; ++p) {
+            if (!plan.split(p)) continue;
+            bool ok = true, any = false;
+            int perSign[2] = {0, 0};
+            for (std::size_t gi = 0; gi < net.groups.size() && ok; ++gi) {
+                const auto& g = net.groups[gi];
+                if (g.pre == p) ok = false;  // not a sink
+                if (g.post != p) continue;
+                any = true;
+                const auto& pre = net.pops[g.pre];
+                ok = ok && g.dense && !g.plastic && plan.split(g.pre) && g.pre != p &&
+                     g.preOffset == 0 && g.preCount == pre.n && pre.n >= heavyThreshold &&
+                     g.nPost % 4 == 0 && g.nPost <= 128 && ++perSign[g.inhibitory ? 1 : 0] == 1;
+            }
+            if (!ok || !any) continue;
+            plan.pipeSink[p] = 1;
+            plan.chunk[p] = net.pops[p].n;  // rank 0 owns the whole population
+            auto& b = plan.bounds[p];
+            b.assign(R + 1, net.pops[p].n);
+            b[0] = 0;
+            for (std::size_t gi = 0; gi < net.groups.size(); ++gi)
+                if (net.groups[gi].post == p) plan.rowSplit[gi] = 1;
+        }
+    }
     return plan;
 }
 
@@ -80,6 +111,19 @@ HostNet shard_net(const HostNet& net, const ShardPlan& plan, int rank, ShardStor
     }
     for (std::size_t gi = 0; gi < net.groups.size(); ++gi) {
         const auto& g = net.groups[gi];
+        if (!plan.rowSplit.empty() && plan.rowSplit[gi]) {
+            // this rank's own pre rows, every post column (dense, whole pre range)
+            auto& G = out.groups[gi];
+            const int lo = plan.bounds[g.pre][rank], hi = plan.bounds[g.pre][rank + 1];
+            G.rowSplit = true;
+            G.preLo = lo;
+            G.nPre = G.preCount = hi - lo;
+            G.preOffset = 0;
+            auto& w = store.f.emplace_back(g.W + static_cast<std::size_t>(lo) * g.nPost,
+                                           g.W + static_cast<std::size_t>(hi) * g.nPost);
+            G.W = w.data();
+            continue;
+        }
         if (!plan.split(g.post)) continue;
         auto& G = out.groups[gi];
         const int lo = plan.bounds[g.post][rank], hi = plan.bounds[g.post][rank + 1];
