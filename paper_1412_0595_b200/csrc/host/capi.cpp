@@ -268,7 +268,9 @@ ssb::EngineConfig to_config(const ssb_engine_opts* o) {
 
 // Population kinds, sizes and group endpoints of a spec (no matrices): what
 // the shard plan reads.
-ssb::HostNet skeleton(const NetworkSpec& spec) {
+// The host network without matrices: what plan_shards decides on (the
+// storage each group gets under `mode`, its pre window and post size).
+ssb::HostNet skeleton(const NetworkSpec& spec, StorageMode mode = StorageMode::FromSpec) {
     ssb::HostNet net;
     for (const auto& p : spec.populations) {
         ssb::HostPop hp;
@@ -290,6 +292,18 @@ ssb::HostNet skeleton(const NetworkSpec& spec) {
         hg.name = g.name;
         hg.pre = index(g.pre);
         hg.post = index(g.post);
+        hg.preOffset = g.preOffset;
+        hg.preCount = group_pre_count(g, spec.populations[hg.pre].size);
+        hg.nPre = hg.preCount;
+        hg.nPost = spec.populations[hg.post].size;
+        hg.outDegree = g.outDegree;
+        hg.inhibitory = g.sign == SynapseSign::Inhibitory;
+        hg.plastic = g.stdp.enabled;
+        hg.dense = mode == StorageMode::ForceDense    ? true
+                   : mode == StorageMode::ForceSparse ? false
+                   : mode == StorageMode::Auto
+                       ? static_cast<double>(g.outDegree) >= auto_dense_threshold() * hg.nPost
+                       : g.storage == StorageKind::Dense;
         net.groups.push_back(hg);
     }
     return net;
@@ -610,7 +624,7 @@ int ssb_shard_group(const ssb_net_desc* net, int32_t storage_mode, int32_t group
         if (group < 0 || group >= static_cast<int32_t>(spec.synapses.size()))
             throw SpecError("group index out of range");
         if (world < 1) throw SpecError("world must be >= 1");
-        ssb::HostNet skel = skeleton(spec);
+        ssb::HostNet skel = skeleton(spec, to_mode(storage_mode));
         const ssb::ShardPlan plan = ssb::plan_shards(skel, world, min_size > 0 ? min_size : 64);
         std::optional<DenseMatrix> d;
         std::optional<CrsMatrix> s;

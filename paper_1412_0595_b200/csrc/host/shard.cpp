@@ -111,6 +111,8 @@ HostNet shard_net(const HostNet& net, const ShardPlan& plan, int rank, ShardStor
     }
     for (std::size_t gi = 0; gi < net.groups.size(); ++gi) {
         const auto& g = net.groups[gi];
+        // (a skeleton's groups without matrices -- ssb_shard_group builds one)
+        if (g.dense ? !g.W : !g.rowStart) continue;
         if (!plan.rowSplit.empty() && plan.rowSplit[gi]) {
             // this rank's own pre rows, every post column (dense, whole pre range)
             auto& G = out.groups[gi];

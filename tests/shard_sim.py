@@ -1,9 +1,12 @@
 """One rank of a split run, restated on the CPU with numpy (test infrastructure).
 
 Checks the multi-GPU decomposition itself -- which populations a world
-splits, each rank's column slices (both taken from the product library's host
-code: ssb_shard_plan / ssb_shard_group) and the spike exchange in rank order
--- with a real multi-process collective (torch.distributed, gloo).  The
+splits, each rank's column (or row) slices (both taken from the product
+library's host code: ssb_shard_plan / ssb_shard_group), the spike exchange in
+rank order and the rank pipeline of row-split groups (each rank continues the
+previous rank's partial sums over its own pre rows, the last rank hands them
+to rank 0, which owns the sink population) -- with real multi-process
+communication (torch.distributed, gloo).  The
 per-step arithmetic follows the reference step (engine.cpp:316-356) in numpy
 float32, which rounds every operation like the reference's -ffp-contract=off
 build; the merged raster is compared with the unsplit oracle in the test.
@@ -19,9 +22,11 @@ from paper_1412_0595_b200 import synscale as S
 
 class ShardSim:
     def __init__(self, spec: S.NetworkSpec, mode: S.StorageMode, world: int, rank: int,
-                 exchange, min_size: int = 0):
-        """exchange(list_of_local_arrays) -> list (per rank) of those lists."""
+                 exchange, min_size: int = 0, send=None, recv=None):
+        """exchange(list_of_local_arrays) -> list (per rank) of those lists;
+        send(float32 array, dst) / recv(n, src): the pipeline's point to point."""
         self.spec, self.world, self.rank, self.exchange = spec, world, rank, exchange
+        self.send, self.recv = send, recv
         self.plan = S.shard_plan(spec, world, min_size)
         self.dt = np.float32(spec.dtMs)
         self.steps = max(1, math.ceil(spec.durationMs / spec.dtMs - 1e-9))
@@ -53,9 +58,16 @@ class ShardSim:
         self.groups = []
         for gi, g in enumerate(spec.synapses):
             kind, m = S.shard_group(spec, gi, world, rank, mode, min_size)
-            self.groups.append({"pre": spec.pop_index(g.pre), "post": spec.pop_index(g.post),
+            pre, post = spec.pop_index(g.pre), spec.pop_index(g.post)
+            pb, qb = self.plan[g.pre], self.plan[g.post]
+            # row split (rank pipeline): rank 0 owns the post population, this
+            # rank holds its own pre rows x every post column
+            rows = (kind == "dense" and pb is not None and qb is not None and world > 1 and
+                    qb[1] == spec.populations[post].size and
+                    m.shape == (pb[rank + 1] - pb[rank], spec.populations[post].size))
+            self.groups.append({"pre": pre, "post": post,
                                 "inh": g.sign == S.SynapseSign.Inhibitory,
-                                "off": g.preOffset, "kind": kind, "m": m})
+                                "off": g.preOffset, "kind": kind, "m": m, "rows": rows})
         self.events = []  # (step, pop, neuron), global ids
         self.t = 0
         self.flagged = 0
@@ -99,6 +111,16 @@ class ShardSim:
             st["inh"][:] = 0
         for g in self.groups:  # propagate in spec order (engine.cpp:343-355)
             acc = self.pops[g["post"]]["inh" if g["inh"] else "exc"]
+            if g["rows"]:  # rank pipeline over this rank's own (local) spiking rows
+                n = g["m"].shape[1]
+                part = (np.zeros(n, np.float32) if self.rank == 0
+                        else self.recv(n, self.rank - 1))
+                for r in local[g["pre"]]:
+                    part += g["m"][r]
+                self.send(part, self.rank + 1 if self.rank < self.world - 1 else 0)
+                if self.rank == 0:
+                    acc += self.recv(n, self.world - 1)  # acc is +0: exact
+                continue
             rows = spikes[g["pre"]] - g["off"]
             if g["kind"] == "dense":
                 W = g["m"]

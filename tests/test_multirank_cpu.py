@@ -13,6 +13,7 @@ import sys
 
 import numpy as np
 import pytest
+import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
@@ -41,7 +42,10 @@ def _worker(rank, world, port, out_path):
         assert plan["pn"] is None and plan["lhi"] is None  # small / Poisson: replicated
         assert plan["kc"] is not None and plan["dn"] is not None
 
-        # the ranks' column slices tile every group exactly
+        # the rank pipeline: dn (fed only by kc_dn) is owned by rank 0 and
+        # kc_dn is split by kc rows
+        assert plan["dn"] == [0] + [100] * world
+        # the ranks' column (row) slices tile every group exactly
         for gi, g in enumerate(spec.synapses):
             kind, m = S.shard_group(spec, gi, world, rank, mode)
             parts = [None] * world
@@ -49,7 +53,9 @@ def _worker(rank, world, port, out_path):
             fk, full = S.build_group(spec, gi, mode)
             assert all(k == fk for k, _ in parts)
             b = plan[g.post]
-            if b is None:  # whole post population: every rank holds the whole group
+            if g.name == "kc_dn":  # rows of each rank's kc range, in rank order
+                assert np.array_equal(np.concatenate([p for _, p in parts], axis=0), full)
+            elif b is None:  # whole post population: every rank holds the whole group
                 for _, p in parts:
                     if fk == "dense":
                         assert np.array_equal(p, full)
@@ -71,7 +77,15 @@ def _worker(rank, world, port, out_path):
             dist.all_gather_object(got, local)
             return got
 
-        sim = ShardSim(spec, mode, world, rank, exchange)
+        def send(arr, dst):
+            dist.send(torch.from_numpy(np.ascontiguousarray(arr, np.float32)), dst)
+
+        def recv(n, src):
+            t = torch.empty(n, dtype=torch.float32)
+            dist.recv(t, src)
+            return t.numpy()
+
+        sim = ShardSim(spec, mode, world, rank, exchange, send=send, recv=recv)
         events = np.array(sim.run(), np.int64).reshape(-1, 3)
         flagged = [None] * world
         dist.all_gather_object(flagged, sim.flagged)
