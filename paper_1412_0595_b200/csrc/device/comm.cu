@@ -27,6 +27,8 @@ struct Nccl {
     ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
 };
 
 Nccl& nccl() {
@@ -47,6 +49,8 @@ Nccl& nccl() {
         n.send = reinterpret_cast<decltype(n.send)>(dlsym(n.lib, "ncclSend"));
         n.recv = reinterpret_cast<decltype(n.recv)>(dlsym(n.lib, "ncclRecv"));
         n.commSplit = reinterpret_cast<decltype(n.commSplit)>(dlsym(n.lib, "ncclCommSplit"));
+        n.groupStart = reinterpret_cast<decltype(n.groupStart)>(dlsym(n.lib, "ncclGroupStart"));
+        n.groupEnd = reinterpret_cast<decltype(n.groupEnd)>(dlsym(n.lib, "ncclGroupEnd"));
     });
     if (!n.lib || !n.getUniqueId || !n.commInitRank || !n.allGather || !n.allReduce)
         throw DeviceError("NCCL (libnccl.so.2) is not available for a multi-GPU run");
@@ -159,9 +163,36 @@ void comm_selftest(int device) {
     cudaFree(send);
     cudaFree(recv);
     cudaFree(sum);
-    cudaStreamDestroy(s);
     if (back != h) throw DeviceError("NCCL self-test: all-gather returned wrong words");
     if (got != 7) throw DeviceError("NCCL self-test: all-reduce returned a wrong sum");
+    // the rank pipeline's pieces: a split communicator and fp32 send / recv
+    // (to this rank itself, in one group), captured in a graph
+    auto split = comm.split();
+    float* a = nullptr;
+    float* b = nullptr;
+    ck(cudaMalloc(&a, n * 4), "cudaMalloc");
+    ck(cudaMalloc(&b, n * 4), "cudaMalloc");
+    std::vector<float> hf(n), bf(n);
+    for (int i = 0; i < n; ++i) hf[i] = 0.25f * static_cast<float>(i) - 3.0f;
+    ck(cudaMemcpy(a, hf.data(), n * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
+    ck(cudaMemset(b, 0, n * 4), "cudaMemset");
+    if (!nccl().groupStart || !nccl().groupEnd) throw DeviceError("ncclGroupStart/End unavailable");
+    ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    nck(nccl().groupStart(), "ncclGroupStart");
+    split->send_f32(a, n, 0, s);
+    split->recv_f32(b, n, 0, s);
+    nck(nccl().groupEnd(), "ncclGroupEnd");
+    ck(cudaStreamEndCapture(s, &g), "cudaStreamEndCapture");
+    ck(cudaGraphInstantiate(&ge, g, 0), "cudaGraphInstantiate");
+    ck(cudaGraphLaunch(ge, s), "cudaGraphLaunch");
+    ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    ck(cudaMemcpy(bf.data(), b, n * 4, cudaMemcpyDeviceToHost), "cudaMemcpy");
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaFree(a);
+    cudaFree(b);
+    cudaStreamDestroy(s);
+    if (bf != hf) throw DeviceError("NCCL self-test: send / recv returned wrong values");
 }
 
 }  // namespace ssb
