@@ -280,6 +280,8 @@ struct DeviceEngine::Impl {
         int tileN = 0;              // neurons per block
         int quad = 0;               // CondLif: neurons per thread of the quad kernel (0: tile kernel)
         bool globalUse = false;     // some consumer group reads its global spikes (not row-split)
+        int tailGroup = -1;         // plastic group whose post population this is (plastic.cuh)
+        float* tailExc = nullptr;   // [2][n] the tail kernel's fold results
         bool pipeSource = false;    // a row-split group reads its local lists
         int chunk = 1;              // steps per phase-A/phase-B chunk
         int offIn = 0;              // shared offset of the phase-A inputs
@@ -344,7 +346,11 @@ struct DeviceEngine::Impl {
     // extension F2: plastic groups (step mode), one device view per buffer set
     struct StdpRt {
         int gi = 0, grid = 1, smem = 0;
+        bool tail = false;  // run by the post population's tail kernel, not per step
         ssbk::StdpDev dev[kMaxSets]{};
+        ssbk::TailDev tdev[kMaxSets]{};
+        float* WT = nullptr;  // the tail's transposed weights [nPost][nPre]
+        int tailGrid = 1;     // sink_step_kernel blocks
     };
     std::vector<StdpRt> stdp;
     std::vector<ssbk::GroupDev> groupDev;
@@ -877,7 +883,32 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     // window pipeline's lagged post updates would read stale weights)
     bool plastic = false;
     for (const auto& g : net.groups) plastic = plastic || g.plastic;
-    stepMode = cyclic || cfg.forceStepMode || plastic;
+    // ... unless every plastic group feeds a sink that has no other input: then
+    // the rest of the network keeps its windows and two kernels per window
+    // run the sink and the learning step by step (plastic.cuh)
+    std::vector<int> tailOf(nPops, -1);
+    bool tail = plastic && !cyclic && !cfg.forceStepMode &&
+                !(std::getenv("SSB_PLASTIC_TAIL") && std::string(std::getenv("SSB_PLASTIC_TAIL")) == "0");
+    for (int gi = 0; tail && gi < static_cast<int>(net.groups.size()); ++gi) {
+        const auto& g = net.groups[gi];
+        if (!g.plastic) continue;
+        const int p = g.post;
+        // the window's trace table ([W][nPre] floats) within a quarter of the free memory
+        std::size_t freeB = 0, totalB = 0;
+        CK(cudaMemGetInfo(&freeB, &totalB));
+        const std::size_t xdBytes = static_cast<std::size_t>(cfg.window) * g.nPre * 4;
+        bool ok = net.pops[p].kind == kCondLif && g.pre != p && g.nPost <= ssbk::kTailMaxPost &&
+                  net.pops[p].nGlobal == 0 && xdBytes <= freeB / 4 &&
+                  tailOf[p] < 0;
+        for (const auto& h : net.groups) {
+            if (h.pre == p) ok = false;                // a sink
+            if (h.post == p && &h != &g) ok = false;   // fed by the plastic group alone
+        }
+        if (ok) tailOf[p] = gi;
+        else tail = false;
+    }
+    if (!tail) std::fill(tailOf.begin(), tailOf.end(), -1);
+    stepMode = cyclic || cfg.forceStepMode || (plastic && !tail);
     if (stepMode) {
         order.resize(nPops);
         std::iota(order.begin(), order.end(), 0);
@@ -898,6 +929,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         const auto& hp = net.pops[pi];
         P.kind = hp.kind;
         P.n = hp.n;
+        P.tailGroup = tailOf[pi];
         P.name = hp.name;
         P.sharded = hp.nGlobal > 0;
         P.nGlobal = P.sharded ? hp.nGlobal : hp.n;
@@ -1301,6 +1333,49 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             L.dev[b].postList = pops[g.post].devb[b].list;
             L.dev[b].postCnt = pops[g.post].devb[b].count;
         }
+        auto& Q = pops[g.post];
+        if (Q.tailGroup == static_cast<int>(gi)) {
+            L.tail = true;
+            ssbk::TailDev T{};
+            T.nSink = (g.nPost + ssbk::kSinkCols - 1) / ssbk::kSinkCols;
+            int perSm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, ssbk::sink_step_kernel,
+                                                             ssbk::kSinkThreads, 0));
+            // sink blocks plus background blocks, every block co-resident
+            int want = std::max(T.nSink + 1, smCount);
+            if (const char* e = std::getenv("SSB_TAIL_GRID")) want = std::max(T.nSink + 1, std::atoi(e));
+            L.tailGrid = std::min(want, perSm * smCount);
+            if (L.tailGrid <= T.nSink)
+                throw synscale::SpecError("plastic group '" + g.name + "': too many post neurons");
+            // the weights transposed [nPost][nPre] (the potentiation walks post
+            // columns); ssb_group_weights transposes back
+            std::vector<float> wt(static_cast<std::size_t>(g.nPre) * g.nPost);
+            for (int r = 0; r < g.nPre; ++r)
+                for (int j = 0; j < g.nPost; ++j)
+                    wt[static_cast<std::size_t>(j) * g.nPre + r] = g.W[static_cast<std::size_t>(r) * g.nPost + j];
+            L.WT = upload<float>(wt.data(), wt.size());
+            T.WT = L.WT;
+            T.x = D.x;
+            T.y = D.y;
+            T.xd = alloc<float>(static_cast<std::size_t>(Wmax) * g.nPre);
+            T.nPre = g.nPre;
+            T.nPost = g.nPost;
+            T.preOffset = g.preOffset;
+            T.aPlus = g.aPlus;
+            T.aMinus = g.aMinus;
+            T.decPlus = g.decPlus;
+            T.decMinus = g.decMinus;
+            T.wMax = g.wMax;
+            for (int b = 0; b < nSets; ++b) {
+                L.tdev[b] = T;
+                L.tdev[b].P = Q.devb[b];
+                L.tdev[b].preList = pops[g.pre].devb[b].list;
+                L.tdev[b].preCnt = pops[g.pre].devb[b].count;
+                L.tdev[b].preBits = pops[g.pre].devb[b].bits;
+                L.tdev[b].preN = pops[g.pre].n;
+                L.tdev[b].preWords = pops[g.pre].nwords;
+            }
+        }
         stdp.push_back(L);
     }
 
@@ -1450,6 +1525,30 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
             ssbk::poisson_window_kernel<<<1, 320, inSmem ? bitsBytes : 0, sm>>>(
                 D, W, P.acc[0].mode, P.acc[1].mode, inSmem);
         });
+        edge(sm, sp);
+        return;
+    }
+    if (P.tailGroup >= 0) {  // plastic sink: the window's steps in two kernels (plastic.cuh)
+        for (const auto& L : stdp) {
+            if (L.gi != P.tailGroup) continue;
+            launchStream = sm;
+            const auto& T = L.tdev[b];
+            launch("sink_trace:" + P.name, [&] {
+                ssbk::sink_trace_kernel<<<(T.nPre + 255) / 256, 256, 0, sm>>>(T, W);
+            });
+            launch("sink_step:" + P.name, [&] {
+                cudaLaunchConfig_t lc{};
+                lc.gridDim = dim3(L.tailGrid);
+                lc.blockDim = dim3(ssbk::kSinkThreads);
+                lc.stream = sm;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeCooperative;
+                at[0].val.cooperative = 1;
+                lc.attrs = at;
+                lc.numAttrs = 1;
+                CK(cudaLaunchKernelEx(&lc, ssbk::sink_step_kernel, T, W));
+            });
+        }
         edge(sm, sp);
         return;
     }
@@ -1630,6 +1729,7 @@ void DeviceEngine::Impl::enqueue_tail(int W, int b, cudaStream_t s) {
     }
     // extension F2: learning after the step's propagation (step mode, W = 1)
     for (const auto& L : stdp) {
+        if (L.tail) continue;
         const auto& D = L.dev[b];
         const std::string& nm = groupMeta[L.gi].name;
         launch("stdp_mark:" + nm, [&] { ssbk::stdp_mark_kernel<<<8, 256, 0, s>>>(D); });
@@ -2375,6 +2475,15 @@ bool DeviceEngine::pull_weights(int group, float* dst, std::int64_t count) {
             throw synscale::SpecError("wrong buffer size");
         CK(cudaSetDevice(m.cfg.device));
         CK(cudaStreamSynchronize(m.stream));
+        if (L.tail) {  // the tail kernel's transposed copy holds the current weights
+            std::vector<float> wt(static_cast<std::size_t>(count));
+            CK(cudaMemcpy(wt.data(), L.WT, wt.size() * 4, cudaMemcpyDeviceToHost));
+            for (int r = 0; r < g.preCount; ++r)
+                for (int j = 0; j < g.nPost; ++j)
+                    dst[static_cast<std::size_t>(r) * g.nPost + j] =
+                        wt[static_cast<std::size_t>(j) * g.preCount + r];
+            return true;
+        }
         CK(cudaMemcpy(dst, L.dev[0].W, static_cast<std::size_t>(count) * 4, cudaMemcpyDeviceToHost));
         return true;
     }
