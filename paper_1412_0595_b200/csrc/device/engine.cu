@@ -884,7 +884,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     bool plastic = false;
     for (const auto& g : net.groups) plastic = plastic || g.plastic;
     // ... unless every plastic group feeds a sink that has no other input: then
-    // the rest of the network keeps its windows and two kernels per window
+    // the rest of the network keeps its windows and one cooperative kernel per window
     // run the sink and the learning step by step (plastic.cuh)
     std::vector<int> tailOf(nPops, -1);
     bool tail = plastic && !cyclic && !cfg.forceStepMode &&
@@ -893,12 +893,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         const auto& g = net.groups[gi];
         if (!g.plastic) continue;
         const int p = g.post;
-        // the window's trace table ([W][nPre] floats) within a quarter of the free memory
-        std::size_t freeB = 0, totalB = 0;
-        CK(cudaMemGetInfo(&freeB, &totalB));
-        const std::size_t xdBytes = static_cast<std::size_t>(cfg.window) * g.nPre * 4;
         bool ok = net.pops[p].kind == kCondLif && g.pre != p && g.nPost <= ssbk::kTailMaxPost &&
-                  net.pops[p].nGlobal == 0 && xdBytes <= freeB / 4 &&
+                  net.pops[p].nGlobal == 0 &&
                   tailOf[p] < 0;
         for (const auto& h : net.groups) {
             if (h.pre == p) ok = false;                // a sink
@@ -1357,7 +1353,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             T.WT = L.WT;
             T.x = D.x;
             T.y = D.y;
-            T.xd = alloc<float>(static_cast<std::size_t>(Wmax) * g.nPre);
+            T.x2 = alloc<float>(static_cast<std::size_t>(g.nPre));
             T.nPre = g.nPre;
             T.nPost = g.nPost;
             T.preOffset = g.preOffset;
@@ -1366,6 +1362,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             T.decPlus = g.decPlus;
             T.decMinus = g.decMinus;
             T.wMax = g.wMax;
+            if (const char* e = std::getenv("SSB_TAIL_SKIP")) T.skip = std::atoi(e);
             for (int b = 0; b < nSets; ++b) {
                 L.tdev[b] = T;
                 L.tdev[b].P = Q.devb[b];
@@ -1528,14 +1525,11 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
         edge(sm, sp);
         return;
     }
-    if (P.tailGroup >= 0) {  // plastic sink: the window's steps in two kernels (plastic.cuh)
+    if (P.tailGroup >= 0) {  // plastic sink: the window's steps in one cooperative kernel (plastic.cuh)
         for (const auto& L : stdp) {
             if (L.gi != P.tailGroup) continue;
             launchStream = sm;
             const auto& T = L.tdev[b];
-            launch("sink_trace:" + P.name, [&] {
-                ssbk::sink_trace_kernel<<<(T.nPre + 255) / 256, 256, 0, sm>>>(T, W);
-            });
             launch("sink_step:" + P.name, [&] {
                 cudaLaunchConfig_t lc{};
                 lc.gridDim = dim3(L.tailGrid);

@@ -1,5 +1,5 @@
 """Short fixed workload for ncu: config 3 + STDP on kc_dn (plastic tail kernel).
-    ncu --set full -k regex:sink_window -s 1 -c 1 python scripts/profile_tail.py"""
+    ncu --set full -k regex:sink_step -s 1 -c 1 python scripts/profile_tail.py"""
 import os
 import sys
 
