@@ -351,6 +351,7 @@ struct DeviceEngine::Impl {
         ssbk::TailDev tdev[kMaxSets]{};
         float* WT = nullptr;  // the tail's transposed weights [nPost][nPre]
         int tailGrid = 1;     // sink_step_kernel blocks
+        int tailSmem = 0;
     };
     std::vector<StdpRt> stdp;
     std::vector<ssbk::GroupDev> groupDev;
@@ -884,7 +885,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
     bool plastic = false;
     for (const auto& g : net.groups) plastic = plastic || g.plastic;
     // ... unless every plastic group feeds a sink that has no other input: then
-    // the rest of the network keeps its windows and one cooperative kernel per window
+    // the rest of the network keeps its windows and two kernels per window
     // run the sink and the learning step by step (plastic.cuh)
     std::vector<int> tailOf(nPops, -1);
     bool tail = plastic && !cyclic && !cfg.forceStepMode &&
@@ -893,8 +894,13 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         const auto& g = net.groups[gi];
         if (!g.plastic) continue;
         const int p = g.post;
+        // the window's trace table ([W][nPre] floats) within a quarter of the free memory
+        std::size_t freeB = 0, totalB = 0;
+        CK(cudaMemGetInfo(&freeB, &totalB));
+        const std::size_t xdBytes = static_cast<std::size_t>(cfg.window) * g.nPre * 4;
         bool ok = net.pops[p].kind == kCondLif && g.pre != p && g.nPost <= ssbk::kTailMaxPost &&
-                  net.pops[p].nGlobal == 0 &&
+                  net.pops[p].nGlobal == 0 && cfg.window <= ssbk::kSinkMaxW && xdBytes <= freeB / 4 &&
+                  ssbk::kSinkRing * ((net.pops[g.pre].n + 31) / 32) * 4 <= 160 * 1024 &&
                   tailOf[p] < 0;
         for (const auto& h : net.groups) {
             if (h.pre == p) ok = false;                // a sink
@@ -1334,9 +1340,12 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             L.tail = true;
             ssbk::TailDev T{};
             T.nSink = (g.nPost + ssbk::kSinkCols - 1) / ssbk::kSinkCols;
+            // dynamic shared memory: the ring of L + 2 steps' pre spike bits
+            L.tailSmem = ssbk::kSinkRing * pops[g.pre].nwords * 4;
+            allow_smem(reinterpret_cast<const void*>(&ssbk::sink_step_kernel), L.tailSmem);
             int perSm = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, ssbk::sink_step_kernel,
-                                                             ssbk::kSinkThreads, 0));
+                                                             ssbk::kSinkThreads, L.tailSmem));
             // sink blocks plus background blocks, every block co-resident
             int want = std::max(T.nSink + 1, smCount);
             if (const char* e = std::getenv("SSB_TAIL_GRID")) want = std::max(T.nSink + 1, std::atoi(e));
@@ -1353,7 +1362,9 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             T.WT = L.WT;
             T.x = D.x;
             T.y = D.y;
-            T.x2 = alloc<float>(static_cast<std::size_t>(g.nPre));
+            T.xd = alloc<float>(static_cast<std::size_t>(Wmax) * g.nPre);
+            T.sinkDone = alloc<int>(static_cast<std::size_t>(Wmax));
+            T.bgDone = alloc<int>(static_cast<std::size_t>(Wmax));
             T.nPre = g.nPre;
             T.nPost = g.nPost;
             T.preOffset = g.preOffset;
@@ -1363,6 +1374,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             T.decMinus = g.decMinus;
             T.wMax = g.wMax;
             if (const char* e = std::getenv("SSB_TAIL_SKIP")) T.skip = std::atoi(e);
+            T.fetchRound = 1;
+            if (const char* e = std::getenv("SSB_SINK_FETCH")) T.fetchRound = std::atoi(e);
             for (int b = 0; b < nSets; ++b) {
                 L.tdev[b] = T;
                 L.tdev[b].P = Q.devb[b];
@@ -1525,15 +1538,19 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
         edge(sm, sp);
         return;
     }
-    if (P.tailGroup >= 0) {  // plastic sink: the window's steps in one cooperative kernel (plastic.cuh)
+    if (P.tailGroup >= 0) {  // plastic sink: the window's steps in two kernels (plastic.cuh)
         for (const auto& L : stdp) {
             if (L.gi != P.tailGroup) continue;
             launchStream = sm;
             const auto& T = L.tdev[b];
+            launch("sink_trace:" + P.name, [&] {
+                ssbk::sink_trace_kernel<<<(T.nPre + 255) / 256, 256, 0, sm>>>(T, W);
+            });
             launch("sink_step:" + P.name, [&] {
                 cudaLaunchConfig_t lc{};
                 lc.gridDim = dim3(L.tailGrid);
                 lc.blockDim = dim3(ssbk::kSinkThreads);
+                lc.dynamicSmemBytes = L.tailSmem;
                 lc.stream = sm;
                 cudaLaunchAttribute at[1];
                 at[0].id = cudaLaunchAttributeCooperative;

@@ -11,30 +11,38 @@
 //
 // The rule (DESIGN.md §1 row A22, kernels.cuh stdp_update_kernel) touches a
 // weight w[r][j] at step t in two ways only: row r spiked (w -= aMinus·yd_j,
-// += aPlus·xd_r if j spiked too, clip) or, r silent, column j spiked
-// (w += aPlus·xd_r, clip).  Post column j's input at t + 1 is the fold of
-// the rows spiking at t over column j, in row order, of the weights as they
-// are before step t's learning.  One cooperative kernel per window, one grid
-// barrier per step; phase t:
-//   sink blocks (kSinkCols post columns each, the weights transposed
-//     [nPost][nPre] so a column is contiguous): the post update at t (input:
-//     the block's own fold of t - 1); then for every row spiking at t, the
-//     potentiation still owed from t - 1 (row silent at t - 1, column spiked),
-//     the staged value for the fold, and the row's learning at t; warp 0's
-//     lanes run the column chains over the staged chunks, rows ascending;
-//   background blocks: the potentiation of t - 1 for the rows silent at both
-//     t - 1 and t (contiguous, coalesced along the columns that spiked).
-// The two touch disjoint rows; every weight sees the same operations in the
-// same order as in step mode (potentiation of t - 1 before the row's next
-// learning), so weights and spikes are bit-identical.  After the last step
-// the background blocks apply its potentiation to every silent row.  The pre
-// traces move one step behind, in the background blocks (phase t: x(t-1) from
-// x(t-2), two buffers), so a sink block derives xd(t-1) and xd(t) of its rows
-// from x(t-2) and the row's spike bit at t - 1 with the same operations.
+// += aPlus·xd_r(t) if j spiked too, clip) or, r silent, column j spiked
+// (potentiation: w += aPlus·xd_r(t), clip).  Post column j's input at t + 1
+// is the fold of the rows spiking at t over column j, in row order, of the
+// weights as they are before step t's learning.  The weights are kept
+// transposed [nPost][nPre] (a column contiguous).  One cooperative kernel per
+// window, two roles, no grid-wide barrier:
+//   sink blocks (kSinkCols post columns each): per step t, the post update
+//     (input: the block's own fold of t - 1; the mushroom body's DN fire in
+//     volleys), then for every row spiking at t the potentiations it still
+//     owes from steps t - L .. t - 1 (it was silent since, a column spiked),
+//     the staged value for the fold, and its learning at t; warp 0's lanes run
+//     the column chains over the staged chunks, rows ascending;
+//   background blocks: the potentiation of step s for the rows silent through
+//     s .. s + L (a volley step rewrites the whole matrix), up to L steps behind
+//     the sink blocks -- so a volley's matrix pass overlaps the next steps.
+// Every potentiation of a weight is applied once, by exactly one of the two
+// (the background iff the row stays silent L more steps), and every weight
+// sees the same operations in the same step order as in step mode: weights
+// and spikes are bit-identical.  Ordering: per-step counters (the sink blocks'
+// post updates of step s before the background's step s; the background's step
+// t - L - 1 before a sink block reads rows at t).  At the window's end the
+// background applies the last steps' potentiations to every silent row.  The
+// pre traces' decayed values xd[t][r] come from a table the prepass writes
+// (sink_trace_kernel, [W][nPre]).
 constexpr int kSinkThreads = 512;
 constexpr int kSinkCols = 2;                      // post columns per sink block
-constexpr int kSinkRows = kSinkThreads - 32;      // rows per staged chunk (a producer thread each)
+// producers: the warps off scheduler 0, where warp 0's column chains (the
+// step's critical path) issue alone; a staged chunk is a row per producer
+constexpr int kSinkRows = kSinkThreads / 4 * 3;   // 384
+constexpr int kSinkLag = 4;                       // L: the background's lag in steps
 constexpr int kTailMaxPost = 128;
+constexpr int kSinkMaxW = 256;                    // window steps (the sink blocks' spike history)
 
 struct TailDev {
     PopDev P;                   // the post population (state, spike bits of the set)
@@ -43,194 +51,294 @@ struct TailDev {
     const uint32_t* preBits;    // [W][preWords]
     int preN, preWords, preOffset;
     float* WT;                  // transposed weights [nPost][nPre]
-    float* x;                   // pre traces [nPre]: x(t) for odd t (x(-1): the last window's end)
-    float* x2;                  // pre traces [nPre]: x(t) for even t
+    float* x;                   // pre traces [nPre] (end of the last window)
     float* y;                   // post traces [nPost]
+    float* xd;                  // [Wmax][nPre]: the pre traces' decayed values of each window step
+    int* sinkDone;              // [Wmax]: sink blocks past their post update of step s
+    int* bgDone;                // [Wmax]: background blocks done with step s
     int nPre, nPost, nSink;
     int skip;  // diagnostic (SSB_TAIL_SKIP, timing only): 1 no sink rows, 2 no background
+    int fetchRound;  // round of a step in which the next step's rows are fetched (SSB_SINK_FETCH)
     float aPlus, aMinus, decPlus, decMinus, wMax;
 };
 
-__device__ __forceinline__ float* sink_x(const TailDev& T, int step) {
-    return step & 1 ? T.x : T.x2;
+// xd[t][r] = x_r(t-1)·decPlus for the window's steps, and x moved on
+// (x = xd + 1 where r spiked) -- the pre trace update of stdp_update_kernel,
+// a thread per row.
+__global__ void __launch_bounds__(256) sink_trace_kernel(TailDev T, int W) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= T.nPre) return;
+    const int i = r + T.preOffset;
+    float x = T.x[r];
+    const uint32_t* pb = T.preBits + (i >> 5);
+    float* out = T.xd + r;
+#pragma unroll 8
+    for (int t = 0; t < W; ++t) {
+        const uint32_t word = __ldg(pb + (size_t)t * T.preWords);
+        const float xd = __fmul_rn(x, T.decPlus);
+        out[(size_t)t * T.nPre] = xd;
+        x = (word >> (i & 31)) & 1u ? __fadd_rn(xd, 1.0f) : xd;
+    }
+    T.x[r] = x;
 }
 
 __device__ __forceinline__ float stdp_pot(float w, float xd, float aPlus, float wMax) {
     return stdp_clip(__fadd_rn(w, __fmul_rn(aPlus, xd)), wMax);
 }
 
-__device__ __forceinline__ bool pre_bit(const TailDev& T, int step, int r) {
-    const int i = r + T.preOffset;
-    return (__ldg(T.preBits + (size_t)step * T.preWords + (i >> 5)) >> (i & 31)) & 1u;
+__device__ __forceinline__ uint32_t pre_word(const TailDev& T, int step, int i) {
+    return __ldg(T.preBits + (size_t)step * T.preWords + (i >> 5));
 }
 
-// Phase s + 1 of the background blocks: the pre traces of step s (x(s) from
-// x(s - 1); dst: where x(s) goes) and the potentiation of step s for the rows
-// silent at s (and, ex >= 0, at ex) at the post columns that spiked at s;
-// rows over the background blocks' threads.
-__device__ __forceinline__ void sink_background(const TailDev& T, int s, int ex, float* dst,
-                                                int* s_q, int* s_nq) {
+__device__ __forceinline__ void spin_until(const int* ctr, int target) {
+    while (*reinterpret_cast<const volatile int*>(ctr) < target) __nanosleep(32);
+    __threadfence();
+}
+
+// ---- background blocks -------------------------------------------------------
+// Step s: for post column j that spiked at s, w[r][j] += aPlus·xd_r(s) (clip)
+// for every row r silent at s .. min(s + L, W - 1).  A thread owns fixed work
+// items (four rows x a group of eight post columns) for the whole window, so
+// a weight's potentiations of consecutive steps come from one thread in order.
+__device__ void sink_background(const TailDev& T, int W, uint32_t* s_m) {
     const int nwp = (T.nPost + 31) >> 5;
-    __syncthreads();
-    if (threadIdx.x < nwp) s_q[kTailMaxPost + threadIdx.x] = __ldcg(T.P.bits + (size_t)s * T.P.nwords + threadIdx.x);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int c = 0;
-        for (int i = 0; i < nwp; ++i)
-            for (uint32_t m = s_q[kTailMaxPost + i]; m; m &= m - 1) s_q[c++] = i * 32 + __ffs(m) - 1;
-        *s_nq = c;
-    }
-    __syncthreads();
-    const int nq = *s_nq;
-    const float* src = sink_x(T, s - 1);
     const int nBg = gridDim.x - T.nSink;
     const int tid = (blockIdx.x - T.nSink) * blockDim.x + threadIdx.x, nth = nBg * blockDim.x;
-    const uint32_t* bs = T.preBits + (size_t)s * T.preWords;
-    const uint32_t* be = ex >= 0 ? T.preBits + (size_t)ex * T.preWords : nullptr;
-    if ((T.nPre & 3) == 0 && (T.preOffset & 3) == 0) {
-        // four rows per thread (16-byte accesses): a volley step (most post
-        // neurons spiking together) rewrites the whole matrix
-        // work items (quad, block of eight spiking columns), quads fastest
-        const int nQuad = T.nPre >> 2;
-        const int nKb = max(1, (nq + 7) >> 3);
-        for (int it = tid; it < nQuad * nKb; it += nth) {
-            const int qd = it % nQuad, k0 = (it / nQuad) * 8;
-            const int r = qd << 2, i = r + T.preOffset;
-            const uint32_t spk = (__ldg(bs + (i >> 5)) >> (i & 31)) & 0xfu;
-            uint32_t busy = spk;
-            if (be) busy |= (__ldg(be + (i >> 5)) >> (i & 31)) & 0xfu;
-            const float4 x = __ldcg(reinterpret_cast<const float4*>(src + r));
-            const float xd[4] = {__fmul_rn(x.x, T.decPlus), __fmul_rn(x.y, T.decPlus),
-                                 __fmul_rn(x.z, T.decPlus), __fmul_rn(x.w, T.decPlus)};
-            if (k0 == 0) {
-                float4 xn;
-                xn.x = spk & 1u ? __fadd_rn(xd[0], 1.0f) : xd[0];
-                xn.y = spk & 2u ? __fadd_rn(xd[1], 1.0f) : xd[1];
-                xn.z = spk & 4u ? __fadd_rn(xd[2], 1.0f) : xd[2];
-                xn.w = spk & 8u ? __fadd_rn(xd[3], 1.0f) : xd[3];
-                *reinterpret_cast<float4*>(dst + r) = xn;
-            }
-            if (busy == 0xfu || nq == 0) continue;
-            const float dw[4] = {__fmul_rn(T.aPlus, xd[0]), __fmul_rn(T.aPlus, xd[1]),
-                                 __fmul_rn(T.aPlus, xd[2]), __fmul_rn(T.aPlus, xd[3])};
-            float4 vals[8];  // eight 16-byte loads in flight
+    const bool quads = (T.nPre & 3) == 0 && (T.preOffset & 3) == 0;
+    const int nRowIt = quads ? T.nPre >> 2 : T.nPre;
+    const int nGrp = (T.nPost + 7) >> 3;
+    for (int s = 0; s < W; ++s) {
+        if (threadIdx.x == 0) spin_until(T.sinkDone + s, T.nSink);
+        __syncthreads();
+        if (threadIdx.x < nwp) s_m[threadIdx.x] = __ldcg(T.P.bits + (size_t)s * T.P.nwords + threadIdx.x);
+        __syncthreads();
+        uint32_t any = 0;
+        for (int k = 0; k < nwp; ++k) any |= s_m[k];
+        const int hi = min(s + kSinkLag, W - 1);
+        if (any && !(T.skip & 2)) {
+            for (int it = tid; it < nRowIt * nGrp; it += nth) {
+                const int g = it / nRowIt, ri = it - g * nRowIt;
+                const uint32_t cols = (s_m[g >> 2] >> ((g & 3) * 8)) & 0xffu;
+                if (!cols) continue;
+                if (quads) {
+                    const int r = ri << 2, i = r + T.preOffset;
+                    uint32_t busy = 0;
+                    for (int u = s; u <= hi; ++u) busy |= (pre_word(T, u, i) >> (i & 31)) & 0xfu;
+                    if (busy == 0xfu) continue;
+                    const float4 xd = __ldg(reinterpret_cast<const float4*>(T.xd + (size_t)s * T.nPre + r));
+                    const float dw0 = __fmul_rn(T.aPlus, xd.x), dw1 = __fmul_rn(T.aPlus, xd.y);
+                    const float dw2 = __fmul_rn(T.aPlus, xd.z), dw3 = __fmul_rn(T.aPlus, xd.w);
+                    float4 vals[8];  // the group's spiking columns: every load in flight
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (k0 + u < nq)
-                    vals[u] = __ldcg(reinterpret_cast<const float4*>(T.WT + (size_t)s_q[k0 + u] * T.nPre + r));
+                    for (int u = 0; u < 8; ++u)
+                        if ((cols >> u) & 1u)
+                            vals[u] = __ldcg(reinterpret_cast<const float4*>(T.WT + (size_t)(g * 8 + u) * T.nPre + r));
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (k0 + u >= nq) continue;
-                float4 o = vals[u];
-                o.x = stdp_clip(__fadd_rn(o.x, dw[0]), T.wMax);
-                o.y = stdp_clip(__fadd_rn(o.y, dw[1]), T.wMax);
-                o.z = stdp_clip(__fadd_rn(o.z, dw[2]), T.wMax);
-                o.w = stdp_clip(__fadd_rn(o.w, dw[3]), T.wMax);
-                float* wp = T.WT + (size_t)s_q[k0 + u] * T.nPre + r;
-                if (busy == 0) {
-                    *reinterpret_cast<float4*>(wp) = o;
-                } else {  // a spiking row belongs to the sink blocks this step
-                    if (!(busy & 1u)) wp[0] = o.x;
-                    if (!(busy & 2u)) wp[1] = o.y;
-                    if (!(busy & 4u)) wp[2] = o.z;
-                    if (!(busy & 8u)) wp[3] = o.w;
+                    for (int u = 0; u < 8; ++u) {
+                        if (!((cols >> u) & 1u)) continue;
+                        float4 o = vals[u];
+                        o.x = stdp_clip(__fadd_rn(o.x, dw0), T.wMax);
+                        o.y = stdp_clip(__fadd_rn(o.y, dw1), T.wMax);
+                        o.z = stdp_clip(__fadd_rn(o.z, dw2), T.wMax);
+                        o.w = stdp_clip(__fadd_rn(o.w, dw3), T.wMax);
+                        float* wp = T.WT + (size_t)(g * 8 + u) * T.nPre + r;
+                        if (busy == 0) {
+                            *reinterpret_cast<float4*>(wp) = o;
+                        } else {  // a row spiking by s + L belongs to the sink blocks
+                            if (!(busy & 1u)) wp[0] = o.x;
+                            if (!(busy & 2u)) wp[1] = o.y;
+                            if (!(busy & 4u)) wp[2] = o.z;
+                            if (!(busy & 8u)) wp[3] = o.w;
+                        }
+                    }
+                } else {
+                    const int r = ri, i = r + T.preOffset;
+                    bool busy = false;
+                    for (int u = s; u <= hi; ++u) busy = busy || ((pre_word(T, u, i) >> (i & 31)) & 1u);
+                    if (busy) continue;
+                    const float dw = __fmul_rn(T.aPlus, __ldg(T.xd + (size_t)s * T.nPre + r));
+                    float vals[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if ((cols >> u) & 1u) vals[u] = __ldcg(T.WT + (size_t)(g * 8 + u) * T.nPre + r);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if ((cols >> u) & 1u)
+                            T.WT[(size_t)(g * 8 + u) * T.nPre + r] = stdp_clip(__fadd_rn(vals[u], dw), T.wMax);
                 }
             }
         }
-        return;
-    }
-    for (int r = tid; r < T.nPre; r += nth) {
-        const bool spk = pre_bit(T, s, r);
-        const float xd = __fmul_rn(__ldcg(src + r), T.decPlus);
-        dst[r] = spk ? __fadd_rn(xd, 1.0f) : xd;
-        if (spk || nq == 0 || (ex >= 0 && pre_bit(T, ex, r))) continue;
-        const float dw = __fmul_rn(T.aPlus, xd);
-        for (int k0 = 0; k0 < nq; k0 += 8) {  // eight loads in flight
-            float vals[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (k0 + u < nq) vals[u] = __ldcg(T.WT + (size_t)s_q[k0 + u] * T.nPre + r);
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (k0 + u < nq)
-                    T.WT[(size_t)s_q[k0 + u] * T.nPre + r] = stdp_clip(__fadd_rn(vals[u], dw), T.wMax);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(T.bgDone + s, 1);
         }
     }
 }
 
-// A producer thread's spiking row of a step: its index and whether it was
-// silent at the step before (owed that step's potentiation where a column
-// spiked).  Read-only data, so the next step's rows are fetched while the
-// current step's chains finish; the row's trace x(w-2) and weights load at
-// the step's start.
-struct SinkRow {
-    int r = -1;  // row (local), -1: none
-    bool silentPrev = false;
-};
+// ---- sink blocks -------------------------------------------------------------
+// The pre spike bits of steps w - L .. w + 1 stay in a shared-memory ring
+// (dynamic shared memory, [L + 2][preWords]).
+constexpr int kSinkRing = kSinkLag + 2;  // steps w - L .. w + 1
 
-// xd(w - 1) and xd(w) of a spiking row from x(w - 2) (w = 0: xd(0) from x(-1))
-__device__ __forceinline__ void sink_xd(const TailDev& T, int w, const SinkRow& q, float xs,
-                                        float& xdp, float& xdw) {
-    if (w == 0) {
-        xdp = 0.f;
-        xdw = __fmul_rn(xs, T.decPlus);
-        return;
-    }
-    xdp = __fmul_rn(xs, T.decPlus);
-    xdw = __fmul_rn(q.silentPrev ? xdp : __fadd_rn(xdp, 1.0f), T.decPlus);
+__device__ __forceinline__ bool ring_bit(const uint32_t* ring, int preWords, int step, int i) {
+    return (ring[(step % kSinkRing) * preWords + (i >> 5)] >> (i & 31)) & 1u;
 }
 
-__device__ __forceinline__ SinkRow sink_fetch(const TailDev& T, int w, int e, int cnt) {
+// words [lo, hi) of a step's pre spike bits into the ring, threads i0 + n·k
+__device__ __forceinline__ void ring_load(const TailDev& T, uint32_t* ring, int step, int i0, int n,
+                                          int lo = 0, int hi = 1 << 30) {
+    const uint32_t* pb = T.preBits + (size_t)step * T.preWords;
+    uint32_t* dst = ring + (step % kSinkRing) * T.preWords;
+    hi = min(hi, T.preWords);
+    for (int k0 = lo + i0; k0 < hi; k0 += 8 * n) {  // eight loads in flight
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (k0 + u * n < hi) v[u] = __ldg(pb + k0 + u * n);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (k0 + u * n < hi) dst[k0 + u * n] = v[u];
+    }
+}
+
+// The ring's share of a step's bits in four parts; part p: words
+// [p·part, (p + 1)·part), thread i takes p·part + i + k·kSinkRows
+constexpr int kRingPer = 5;  // words per thread and part (preWords <= 4·5·384)
+
+__device__ __forceinline__ void ring_fetch(const TailDev& T, int step, int i, int p, uint32_t* rv) {
+    const int part = (T.preWords + 3) / 4;
+    const int lo = p * part, hi = min(T.preWords, lo + part);
+    const uint32_t* pb = T.preBits + (size_t)step * T.preWords;
+#pragma unroll
+    for (int u = 0; u < kRingPer; ++u) {
+        const int k = lo + i + u * kSinkRows;
+        rv[u] = k < hi ? __ldg(pb + k) : 0u;
+    }
+}
+
+__device__ __forceinline__ void ring_store(const TailDev& T, uint32_t* ring, int step, int i, int p,
+                                           const uint32_t* rv) {
+    const int part = (T.preWords + 3) / 4;
+    const int lo = p * part, hi = min(T.preWords, lo + part);
+    uint32_t* dst = ring + (step % kSinkRing) * T.preWords;
+#pragma unroll
+    for (int u = 0; u < kRingPer; ++u) {
+        const int k = lo + i + u * kSinkRows;
+        if (k < hi) dst[k] = rv[u];
+    }
+}
+
+// A producer thread's spiking row of a step: its index, its spike bits over
+// the L steps before (bit d - 1: spiked at w - d), and xd at the first step
+// it owes a potentiation for (w - run; xd(w) when it spiked at w - 1).
+// Read-only data, so the next step's rows are fetched while the current
+// step's chains finish; the weights load at the step's start.
+struct SinkRow {
+    int r = -1;  // row (local), -1: none
+    uint32_t hist = 0;
+    float xs = 0.f;
+};
+
+// steps since the row's last spike, at most L and not before the window
+__device__ __forceinline__ int sink_run(uint32_t hist, int w) {
+    return min(hist ? __ffs(hist) - 1 : kSinkLag, w);
+}
+
+// the ring must hold steps w - L .. w - 1
+__device__ __forceinline__ SinkRow sink_fetch_row(const TailDev& T, int w, int rg,
+                                                  const uint32_t* ring) {
     SinkRow q;
-    if (e >= cnt) return q;
-    const int r = __ldg(T.preList + (size_t)w * T.preN + e) - T.preOffset;
+    const int r = rg - T.preOffset;
     if ((unsigned)r >= (unsigned)T.nPre) return q;
     q.r = r;
-    q.silentPrev = w > 0 && !pre_bit(T, w - 1, r);
+    uint32_t h = 0;
+#pragma unroll
+    for (int d = 1; d <= kSinkLag; ++d)
+        if (w - d >= 0) h |= static_cast<uint32_t>(ring_bit(ring, T.preWords, w - d, rg)) << (d - 1);
+    q.hist = h;
+    q.xs = __ldg(T.xd + (size_t)(w - sink_run(h, w)) * T.nPre + r);
     return q;
 }
 
-// Stage a spiking row's values for the fold (after the potentiation owed from
-// w - 1) and store its learning at w (depression, + potentiation where the
-// column spiked at w).
-__device__ __forceinline__ void sink_row(const TailDev& T, int w, const SinkRow& q, float xs,
-                                         const float* vals, int c0, int nc, uint32_t prev,
-                                         uint32_t spk, const float* s_yd, float* stage) {
-    float xdp, xdw;
-    sink_xd(T, w, q, xs, xdp, xdw);
+__device__ __forceinline__ SinkRow sink_fetch(const TailDev& T, int w, int e, int cnt,
+                                              const uint32_t* ring) {
+    if (e >= cnt) return SinkRow{};
+    return sink_fetch_row(T, w, __ldg(T.preList + (size_t)w * T.preN + e), ring);
+}
+
+// the rows of chunks 0 .. kSinkPre - 1 (slot e0 + k·rows): every index load first
+template <int N>
+__device__ __forceinline__ void sink_fetch_all(const TailDev& T, int w, int e0, int rows, int cnt,
+                                               const uint32_t* ring, SinkRow* out) {
+    int rg[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+        rg[k] = e0 + k * rows < cnt ? __ldg(T.preList + (size_t)w * T.preN + e0 + k * rows) : -1;
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+        out[k] = e0 + k * rows < cnt ? sink_fetch_row(T, w, rg[k], ring) : SinkRow{};
+}
+
+// Stage a spiking row's values for the fold -- after the potentiations it
+// owes (steps w - run .. w - 1, silent, where a column spiked: s_hist[s],
+// oldest first; xd(s + 1) = xd(s)·decPlus along a silent run, as the
+// prepass computes it) -- and store its learning at w (depression, +
+// potentiation where the column spiked at w).
+__device__ __forceinline__ void sink_row(const TailDev& T, int w, const SinkRow& q, const float* vals,
+                                         int c0, int nc, uint32_t spk, const float* s_yd,
+                                         const uint32_t* s_hist, float* stage) {
+    // stage[j * kSinkRows]: column j's slot of this row
+    float v[kSinkCols];
+#pragma unroll
+    for (int j = 0; j < kSinkCols; ++j) v[j] = vals[j];
+    float xd = q.xs;
+    for (int s = w - sink_run(q.hist, w); s < w; ++s) {
+        const uint32_t m = s_hist[s];
+#pragma unroll
+        for (int j = 0; j < kSinkCols; ++j)
+            if ((m >> j) & 1u) v[j] = stdp_pot(v[j], xd, T.aPlus, T.wMax);
+        xd = __fmul_rn(xd, T.decPlus);
+    }
 #pragma unroll
     for (int j = 0; j < kSinkCols; ++j) {
-        float val = vals[j];
-        if (q.silentPrev && ((prev >> j) & 1u)) val = stdp_pot(val, xdp, T.aPlus, T.wMax);
-        stage[j] = val;
-        if (q.r < 0 || j >= nc) continue;
-        float nv = __fsub_rn(val, __fmul_rn(T.aMinus, s_yd[j]));
-        if ((spk >> j) & 1u) nv = __fadd_rn(nv, __fmul_rn(T.aPlus, xdw));
+        stage[j * kSinkRows] = v[j];
+        if (j >= nc) continue;
+        float nv = __fsub_rn(v[j], __fmul_rn(T.aMinus, s_yd[j]));
+        if ((spk >> j) & 1u) nv = __fadd_rn(nv, __fmul_rn(T.aPlus, xd));
         T.WT[(size_t)(c0 + j) * T.nPre + q.r] = stdp_clip(nv, T.wMax);
     }
 }
 
-constexpr int kSinkPre = 3;  // chunks of a step whose rows are fetched ahead
+constexpr int kSinkPre = 4;  // chunks of a step whose rows are fetched ahead
+static_assert(kSinkPre == 4, "ring_fetch splits a step's bits in four parts");
 
 __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, int W) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
-    __shared__ float s_stage[2][kSinkRows][kSinkCols];
+    __shared__ __align__(16) float s_stage[2][kSinkCols][kSinkRows];  // a column's rows contiguous
     __shared__ float s_yd[kSinkCols];
-    __shared__ uint32_t s_spk;
+    __shared__ uint32_t s_hist[kSinkMaxW];  // sink: the block's column spikes of each step
     __shared__ int s_cnt;
-    __shared__ int s_q[kTailMaxPost + kTailMaxPost / 32];
-    __shared__ int s_nq;
     __shared__ long long s_red[32];
+    __shared__ unsigned long long s_tw;
+    extern __shared__ uint32_t s_bitRing[];  // sink: pre spike bits [L + 1][preWords]
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const PopDev& P = T.P;
     const int nPre = T.nPre;
-    // the window's post spike bits are OR-ed in by the sink blocks
-    if (blockIdx.x == 0)
+    // the window's post spike bits are OR-ed in by the sink blocks; counters
+    if (blockIdx.x == 0) {
         for (int i = t; i < W * P.nwords; i += blockDim.x) P.bits[i] = 0u;
+        for (int i = t; i < W; i += blockDim.x) T.sinkDone[i] = T.bgDone[i] = 0;
+    }
     const bool sink = static_cast<int>(blockIdx.x) < T.nSink;
+    grid.sync();
+    if (!sink) {
+        sink_background(T, W, reinterpret_cast<uint32_t*>(s_hist));
+        return;
+    }
     const int c0 = blockIdx.x * kSinkCols;
-    const int nc = sink ? min(kSinkCols, T.nPost - c0) : 0;
+    const int nc = min(kSinkCols, T.nPost - c0);
     const bool col = warp == 0 && lane < nc;
     const LifConst lc = lif_const(P);
     float v = 0.f, ge = 0.f, gi = 0.f, y = 0.f, a = 0.f;
@@ -242,146 +350,176 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
         flag = P.nanFlag[c0 + lane] ? 1u : 0u;
         y = T.y[c0 + lane];
     }
-    uint32_t prev = 0;     // the block's columns that spiked at w - 1
-    const int i = t - 32;  // producers (warps 1..): chunk row i
-    SinkRow rec[kSinkPre];
-    if (sink && warp > 0 && W > 0) {
+    const bool producer = (warp & 3) != 0;
+    const int i = ((warp >> 2) * 3 + (warp & 3) - 1) * 32 + lane;  // producers: chunk row i
+    SinkRow rec[kSinkPre], recN[kSinkPre];
+    int nextCnt = 0, pendK = -1, idxN = -1;
+    uint32_t rv[kRingPer];
+    if (producer && W > 0) {
         const int cn = T.skip & 1 ? 0 : T.preCnt[0];
-#pragma unroll
-        for (int kk = 0; kk < kSinkPre; ++kk) rec[kk] = sink_fetch(T, 0, kk * kSinkRows + i, cn);
+        sink_fetch_all<kSinkPre>(T, 0, i, kSinkRows, cn, s_bitRing, rec);
+        ring_load(T, s_bitRing, 0, i, kSinkRows);
     }
-    // SSB_TRACE: block 0 (sink) and block nSink (background) record each step:
-    // {tag | count << 32, post update end | rows end << 32 (ns from the step's
-    // start), barrier end, chain cycles}
-    const bool tr = g_trace != nullptr && t == 0 &&
-                    (blockIdx.x == 0 || static_cast<int>(blockIdx.x) == T.nSink);
+    // SSB_TRACE: block 0 records each step: {tag | count << 32, post update end
+    // | rows end << 32 (ns from the step's start), 0, chain cycles}
+    const bool tr = g_trace != nullptr && t == 0 && blockIdx.x == 0;
     unsigned trBase = 0;
-    if (tr) trBase = atomicAdd(&g_traceN, static_cast<unsigned>(W));
-    grid.sync();
+    if (tr) trBase = atomicAdd(&g_traceN, static_cast<unsigned>(2 * W));
     for (int w = 0; w < W; ++w) {
-        unsigned long long t0 = 0, tA = 0, tB = 0;
+        unsigned long long t0 = 0, tA = 0, tR[4] = {0, 0, 0, 0};
         long long chainCy = 0;
-        int cnt = 0;
-        if (tr) t0 = global_ns();
-        if (sink) {
-            float wv[kSinkPre][kSinkCols];
-            float xs[kSinkPre];
-            if (warp == 0) {
-                const float ex = w == 0 ? (col ? P.excIn[c0 + lane] : 0.f) : a;
-                const float ih = w == 0 ? (col ? P.inhIn[c0 + lane] : 0.f) : 0.f;
-                bool spike = false;
-                if (col) spike = lif_step<true>(lc, ex, ih, v, ge, gi, expMax, bad);
-                const uint32_t m = __ballot_sync(kFull, spike);
-                if (spike) atomicOr(P.bits + (size_t)w * P.nwords + ((c0 + lane) >> 5), 1u << ((c0 + lane) & 31));
-                if (lane == 0) {
-                    s_spk = m;
-                    s_cnt = T.skip & 1 ? 0 : T.preCnt[w];
-                }
-                const float yd = __fmul_rn(y, T.decMinus);
-                if (lane < kSinkCols) s_yd[lane] = yd;
-                y = spike ? __fadd_rn(yd, 1.0f) : yd;
-                a = 0.f;
-            } else {  // meanwhile: the fetched rows' weights (final for this step) and traces
-                const float* xsrc = sink_x(T, w == 0 ? -1 : w - 2);
-#pragma unroll
-                for (int kk = 0; kk < kSinkPre; ++kk) {
-                    xs[kk] = rec[kk].r >= 0 ? __ldcg(xsrc + rec[kk].r) : 0.f;
-#pragma unroll
-                    for (int j = 0; j < kSinkCols; ++j)
-                        wv[kk][j] = rec[kk].r >= 0 && j < nc
-                                        ? __ldcg(T.WT + (size_t)(c0 + j) * nPre + rec[kk].r) : 0.f;
-                }
+        if (tr) {
+            t0 = global_ns();
+            s_tw = t0;
+        }
+        float wv[kSinkPre][kSinkCols];
+        if (warp == 0) {
+            const float ex = w == 0 ? (col ? P.excIn[c0 + lane] : 0.f) : a;
+            const float ih = w == 0 ? (col ? P.inhIn[c0 + lane] : 0.f) : 0.f;
+            bool spike = false;
+            if (col) spike = lif_step<true>(lc, ex, ih, v, ge, gi, expMax, bad);
+            const uint32_t m = __ballot_sync(kFull, spike);
+            if (spike) atomicOr(P.bits + (size_t)w * P.nwords + ((c0 + lane) >> 5), 1u << ((c0 + lane) & 31));
+            if (lane == 0) {
+                s_hist[w] = m;
+                s_cnt = T.skip & 1 ? 0 : T.preCnt[w];
             }
-            __syncthreads();
-            if (tr) tA = global_ns();
-            const uint32_t spk = s_spk;
-            cnt = s_cnt;
-            const int nChunks = (cnt + kSinkRows - 1) / kSinkRows;
-            for (int k = 0; k <= nChunks; ++k) {
-                if (warp == 0) {
-                    if (k > 0 && lane < kSinkCols) {  // the column chains of chunk k - 1
-                        const long long cy0 = tr ? clock64() : 0;
-                        const int n = min(kSinkRows, cnt - (k - 1) * kSinkRows);
-                        const float* sb = &s_stage[(k - 1) & 1][0][lane];
-                        // software-pipelined: the next eight staged values load
-                        // while the current eight add (the chain is the step's floor)
-                        const int n8 = n & ~7;
-                        if (n8 > 0) {
-                            float c[8];
+            const float yd = __fmul_rn(y, T.decMinus);
+            if (lane < kSinkCols) s_yd[lane] = yd;
+            y = spike ? __fadd_rn(yd, 1.0f) : yd;
+            a = 0.f;
+        } else if (producer) {
+            // the background's step w - L - 1 is in (rows spiking now may have
+            // been silent through it); then the fetched rows' weights
+            nextCnt = w + 1 < W && !(T.skip & 1) ? __ldg(T.preCnt + w + 1) : 0;
+            if (w > kSinkLag) {
+                if (t == 32) {
+                    spin_until(T.bgDone + (w - kSinkLag - 1), gridDim.x - T.nSink);
+                    if (g_trace) s_tw = global_ns();
+                }
+                asm volatile("bar.sync 1, %0;" ::"r"(kSinkRows));
+            }
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) c[u] = sb[u * kSinkCols];
-                            for (int q = 8; q < n8; q += 8) {
-                                float d[8];
+            for (int kk = 0; kk < kSinkPre; ++kk)
 #pragma unroll
-                                for (int u = 0; u < 8; ++u) d[u] = sb[(q + u) * kSinkCols];
-#pragma unroll
-                                for (int u = 0; u < 8; ++u) a = __fadd_rn(a, c[u]);
-#pragma unroll
-                                for (int u = 0; u < 8; ++u) c[u] = d[u];
-                            }
-#pragma unroll
-                            for (int u = 0; u < 8; ++u) a = __fadd_rn(a, c[u]);
+                for (int j = 0; j < kSinkCols; ++j)
+                    wv[kk][j] = rec[kk].r >= 0 && j < nc
+                                    ? __ldcg(T.WT + (size_t)(c0 + j) * nPre + rec[kk].r) : 0.f;
+        }
+        __syncthreads();
+        if (t == 32) {  // the block's post spikes of w are out (off warp 0's path)
+            __threadfence();
+            atomicAdd(T.sinkDone + w, 1);
+        }
+        if (tr) tA = global_ns();
+        const uint32_t spk = s_hist[w];
+        const int cnt = s_cnt;
+        const int nChunks = (cnt + kSinkRows - 1) / kSinkRows;
+        for (int k = 0; k <= nChunks; ++k) {
+            if (warp == 0) {
+                if (k > 0 && lane < kSinkCols) {  // the column chains of chunk k - 1
+                    const long long cy0 = tr ? clock64() : 0;
+                    const int n = min(kSinkRows, cnt - (k - 1) * kSinkRows);
+                    const float* sb = &s_stage[(k - 1) & 1][lane][0];
+                    // four staged values per 16-byte load, the next four loading
+                    // while the current four add (the chain is the step's floor)
+                    const int n4 = n & ~3;
+                    if (n4 > 0) {
+                        float4 c = *reinterpret_cast<const float4*>(sb);
+                        for (int q = 4; q < n4; q += 4) {
+                            const float4 d = *reinterpret_cast<const float4*>(sb + q);
+                            a = __fadd_rn(a, c.x);
+                            a = __fadd_rn(a, c.y);
+                            a = __fadd_rn(a, c.z);
+                            a = __fadd_rn(a, c.w);
+                            c = d;
                         }
-                        for (int q = n8; q < n; ++q) a = __fadd_rn(a, sb[q * kSinkCols]);
-                        if (tr) {
-                            const float aa = a;
-                            asm volatile("" ::"f"(aa));
-                            chainCy += clock64() - cy0;
-                        }
+                        a = __fadd_rn(a, c.x);
+                        a = __fadd_rn(a, c.y);
+                        a = __fadd_rn(a, c.z);
+                        a = __fadd_rn(a, c.w);
                     }
-                } else {
-                    if (k < nChunks) {
-                        const int e = k * kSinkRows + i;
-                        float* stage = &s_stage[k & 1][i][0];
-                        if (k < kSinkPre) {
+                    for (int q = n4; q < n; ++q) a = __fadd_rn(a, sb[q]);
+                    if (tr) {
+                        const float aa = a;
+                        asm volatile("" ::"f"(aa));
+                        chainCy += clock64() - cy0;
+                    }
+                }
+            } else if (producer) {
+                if (k < nChunks) {
+                    const int e = k * kSinkRows + i;
+                    float* stage = &s_stage[k & 1][0][i];
+                    if (k < kSinkPre) {
 #pragma unroll
-                            for (int kk = 0; kk < kSinkPre; ++kk)
-                                if (kk == k && e < cnt)
-                                    sink_row(T, w, rec[kk], xs[kk], wv[kk], c0, nc, prev, spk, s_yd, stage);
-                        } else if (e < cnt) {  // beyond the fetched chunks: on demand
-                            const SinkRow q = sink_fetch(T, w, e, cnt);
+                        for (int kk = 0; kk < kSinkPre; ++kk)
+                            if (kk == k && e < cnt) {
+                                if (rec[kk].r >= 0)
+                                    sink_row(T, w, rec[kk], wv[kk], c0, nc, spk, s_yd, s_hist, stage);
+                                else
+                                    for (int j = 0; j < kSinkCols; ++j) stage[j * kSinkRows] = 0.f;
+                            }
+                    } else if (e < cnt) {  // beyond the fetched chunks: on demand
+                        const SinkRow q = sink_fetch(T, w, e, cnt, s_bitRing);
+                        if (q.r >= 0) {
                             float vals[kSinkCols];
 #pragma unroll
                             for (int j = 0; j < kSinkCols; ++j)
-                                vals[j] = q.r >= 0 && j < nc ? __ldcg(T.WT + (size_t)(c0 + j) * nPre + q.r) : 0.f;
-                            const float x0 = q.r >= 0 ? __ldcg(sink_x(T, w == 0 ? -1 : w - 2) + q.r) : 0.f;
-                            sink_row(T, w, q, x0, vals, c0, nc, prev, spk, s_yd, stage);
+                                vals[j] = j < nc ? __ldcg(T.WT + (size_t)(c0 + j) * nPre + q.r) : 0.f;
+                            sink_row(T, w, q, vals, c0, nc, spk, s_yd, s_hist, stage);
+                        } else {
+                            for (int j = 0; j < kSinkCols; ++j) stage[j * kSinkRows] = 0.f;
                         }
                     }
-                    // after the last chunk: the next step's rows (read-only data)
-                    if (k == max(nChunks - 1, 0) && w + 1 < W) {
-                        const int cn = T.skip & 1 ? 0 : __ldg(T.preCnt + w + 1);
+                }
+                // in each round's slack (the chains are the longer part), a
+                // share of the next step's rows and pre spike bits (read-only):
+                // round k issues the loads of chunk k's row and ring part k,
+                // round k + 1 consumes them; the last round finishes the rest
+                if (w + 1 < W) {
+                    if (pendK >= 0) {
 #pragma unroll
                         for (int kk = 0; kk < kSinkPre; ++kk)
-                            rec[kk] = sink_fetch(T, w + 1, kk * kSinkRows + i, cn);
+                            if (kk == pendK) recN[kk] = idxN >= 0 ? sink_fetch_row(T, w + 1, idxN, s_bitRing) : SinkRow{};
+                        ring_store(T, s_bitRing, w + 1, i, pendK, rv);
+                        pendK = -1;
+                    }
+                    if (k < nChunks && k < kSinkPre) {
+                        const int e = k * kSinkRows + i;
+                        idxN = e < nextCnt ? __ldg(T.preList + (size_t)(w + 1) * T.preN + e) : -1;
+                        ring_fetch(T, w + 1, i, k, rv);
+                        pendK = k;
+                    } else if (k == nChunks) {
+#pragma unroll
+                        for (int kk = 0; kk < kSinkPre; ++kk)
+                            if (kk >= k) {
+                                recN[kk] = sink_fetch(T, w + 1, kk * kSinkRows + i, nextCnt, s_bitRing);
+                                ring_fetch(T, w + 1, i, kk, rv);
+                                ring_store(T, s_bitRing, w + 1, i, kk, rv);
+                            }
                     }
                 }
-                __syncthreads();
             }
-            prev = spk;
-            if (tr) tB = global_ns();
-        } else if (w > 0) {
-            if (!(T.skip & 2)) sink_background(T, w - 1, w, sink_x(T, w - 1), s_q, &s_nq);
-            if (tr) {
-                tA = tB = global_ns();
-                cnt = s_nq;
-            }
-        } else if (tr) {
-            tA = tB = global_ns();
+            // the last round needs no barrier: warp 0 goes on to the next
+            // post update, the producers to the next step's weights, and the
+            // step's first barrier joins them before any chunk is restaged
+            if (k < nChunks) __syncthreads();
+            if (tr && k < 4) tR[k] = global_ns() - t0;
         }
-        grid.sync();
-        if (tr) {
-            unsigned long long* e = g_trace + 4ull * (trBase + w);
-            if (trBase + w < g_traceCap) {
-                e[0] = (sink ? 0x5100ull : 0x5110ull) | (static_cast<unsigned long long>(cnt) << 32);
-                e[1] = (tA - t0) | ((tB - t0) << 32);
-                e[2] = global_ns() - t0;
-                e[3] = static_cast<unsigned long long>(chainCy);
-            }
+#pragma unroll
+        for (int kk = 0; kk < kSinkPre; ++kk) rec[kk] = recN[kk];
+        if (tr && trBase + 2 * w + 1 < g_traceCap) {
+            unsigned long long* e = g_trace + 4ull * (trBase + 2 * w);
+            e[0] = 0x5100ull | (static_cast<unsigned long long>(cnt) << 32);
+            e[1] = (tA - t0) | ((global_ns() - t0) << 32);
+            e[2] = s_tw - t0;
+            e[3] = static_cast<unsigned long long>(chainCy);
+            e[4] = 0x5101ull;
+            e[5] = tR[0] | (tR[1] << 32);
+            e[6] = tR[2];
+            e[7] = tR[3];
         }
     }
-    // the last step's potentiation and traces (x(W-1) where the next window expects x(-1))
-    if (!sink && W > 0 && !(T.skip & 2)) sink_background(T, W - 1, -1, T.x, s_q, &s_nq);
     // ---- end of window: post state, next window's first input, traces
     if (col) {
         const int j = c0 + lane;

@@ -40,17 +40,19 @@ def stat(name, d):
 
 
 s = tag == 0x5100
-b = tag == 0x5110
 print("steps", int(s.sum()), "spiking rows per step", cnt[s].mean())
-stat("step (sink block)", tS[s])
+stat("step (sink block 0)", tB[s])
 stat("sink post update", tA[s])
+stat("  background wait end", tS[s])
 stat("sink rows", tB[s] - tA[s])
-stat("sink barrier", tS[s] - tB[s])
-stat("background work", tB[b])
-nq = cnt[b]
-for lo, hi in [(0, 0), (1, 4), (5, 20), (21, 60), (61, 1000)]:
-    m = (nq >= lo) & (nq <= hi)
-    if m.any():
-        print(f"   post spikes {lo:3d}-{hi:4d}: {m.mean() * 100:5.1f}% of steps, background {tB[b][m].mean():7.3f} us")
-stat("background barrier", tS[b] - tB[b])
 print(f"chain: {cy[s].sum() / cnt[s].sum():.2f} cycles per row")
+r = tag == 0x5101
+if r.any():
+    r0 = (rec[r, 1] & 0xffffffff).astype(np.float64) / 1e3
+    r1 = (rec[r, 1] >> 32).astype(np.float64) / 1e3
+    r2 = rec[r, 2].astype(np.float64) / 1e3
+    r3 = rec[r, 3].astype(np.float64) / 1e3
+    stat("round 0 end", r0)
+    stat("round 1 end", r1)
+    stat("round 2 end", r2)
+    stat("round 3 end", r3)
