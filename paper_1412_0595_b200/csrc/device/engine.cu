@@ -335,6 +335,10 @@ struct DeviceEngine::Impl {
     }
     int Wmax = 1;
     bool stepMode = false;
+    // small recurrent networks: one block runs each window (cyclic.cuh)
+    bool cycBlock = false;
+    ssbk::CycDev* cycDev[kMaxSets] = {};
+    std::vector<const long long*> rowPtrDev;  // CRS row pointers per group (device)
     int smCount = 148;
     // SMs the block-size choice leaves to the other populations' kernels,
     // which run concurrently in the window graphs (~10% with several
@@ -534,6 +538,7 @@ struct DeviceEngine::Impl {
     std::int64_t pre_launch(int W, int M);
     void post_launch(int W, int M, std::int64_t add);
     void enqueue_tail(int W, int b, cudaStream_t s);
+    void enqueue_cyclic(int W, int M);
     void enqueue_windows(int W, int M);
     void run_windows(int W, int M);
     void flush_raster(bool wait = false);
@@ -915,8 +920,34 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         order.resize(nPops);
         std::iota(order.begin(), order.end(), 0);
     }
-    Wmax = stepMode ? 1 : std::max(1, cfg.window);
-    if (!stepMode && net.steps > 0) Wmax = static_cast<int>(std::min<std::int64_t>(Wmax, net.steps));
+    // a small recurrent network keeps windows: one block advances every
+    // population step by step (the step-mode plans are built but not launched)
+    if (cyclic && !plastic && !cfg.forceStepMode &&
+        !(std::getenv("SSB_CYCLIC_BLOCK") && std::string(std::getenv("SSB_CYCLIC_BLOCK")) == "0")) {
+        bool ok = nPops <= ssbk::kCycMaxPops &&
+                  static_cast<int>(net.groups.size()) <= ssbk::kCycMaxGroups;
+        int pad = 0, nAcc = 0, rows = 0;
+        for (int pi = 0; pi < nPops; ++pi) {
+            const auto& hp = net.pops[pi];
+            ok = ok && hp.nGlobal == 0 &&
+                 (hp.kind == kIzhikevich || hp.kind == kCondLif || hp.kind == kPoisson);
+            pad += (hp.n + 31) / 32 * 32;
+            for (int a = 0; a < 2; ++a) {
+                bool any = false;
+                for (const auto& g : net.groups)
+                    any = any || (g.post == pi && (g.inhibitory ? 1 : 0) == a && hp.kind != kPoisson);
+                if (any) nAcc += hp.n;
+            }
+        }
+        for (const auto& g : net.groups) {
+            rows += g.preCount;
+            ok = ok && !g.rowSplit && g.preCount < (1 << 24);
+        }
+        cycBlock = ok && pad <= ssbk::kCycMaxN && nAcc <= ssbk::kCycMaxAcc && rows <= ssbk::kCycMaxRows;
+    }
+    Wmax = stepMode && !cycBlock ? 1 : std::max(1, cfg.window);
+    if ((!stepMode || cycBlock) && net.steps > 0)
+        Wmax = static_cast<int>(std::min<std::int64_t>(Wmax, net.steps));
 
     // accumulator plans
     pops.resize(nPops);
@@ -1145,6 +1176,10 @@ void DeviceEngine::Impl::build(const HostNet& net) {
                 P.devb[b].bits = alloc<uint32_t>(static_cast<std::size_t>(Wmax) * P.nwords);
                 P.devb[b].list = alloc<int>(static_cast<std::size_t>(Wmax) * n);
                 P.devb[b].count = alloc<int>(static_cast<std::size_t>(Wmax));
+                // the one-block path draws a window's noise while the block
+                // kernel runs the previous window
+                if (cycBlock && hp.kind == kIzhikevich)
+                    P.devb[b].noiseIn = alloc<float>(static_cast<std::size_t>(Wmax) * n);
             }
             for (int a = 0; a < 2; ++a) {
                 P.accb[b][a] = P.acc[a];
@@ -1190,6 +1225,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
 
     // groups
     groupDev.resize(net.groups.size());
+    rowPtrDev.assign(net.groups.size(), nullptr);
     for (std::size_t gi = 0; gi < net.groups.size(); ++gi) {
         const auto& g = net.groups[gi];
         auto& G = groupDev[gi];
@@ -1239,6 +1275,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             G.fullRows = g.nnz == static_cast<std::int64_t>(g.preCount) * g.nPost ? 1 : 0;
             long long* rs = upload<long long>(
                 reinterpret_cast<const long long*>(g.rowStart), static_cast<std::size_t>(g.nPre) + 1);
+            rowPtrDev[gi] = rs;
             int* seg = alloc<int>(static_cast<std::size_t>(g.preCount) * (G.nTiles + 1));
             const long long total = static_cast<long long>(g.preCount) * (G.nTiles + 1);
             if (total > 0) {
@@ -1387,6 +1424,47 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             }
         }
         stdp.push_back(L);
+    }
+
+    if (cycBlock) {  // the block kernel's view of the network, per window-buffer set
+        ssbk::CycDev C{};
+        C.nPops = nPops;
+        C.nGroups = static_cast<int>(net.groups.size());
+        int base = 0, acc = 0;
+        for (int pi = 0; pi < nPops; ++pi) {
+            C.pops[pi].base = base;
+            base += (pops[pi].n + 31) / 32 * 32;
+            for (int a = 0; a < 2; ++a) {
+                bool any = false;
+                for (const auto& g : net.groups)
+                    any = any || (g.post == pi && (g.inhibitory ? 1 : 0) == a &&
+                                  pops[pi].kind != kPoisson);
+                C.pops[pi].acc[a] = any ? acc : -1;
+                if (any) acc += pops[pi].n;
+            }
+        }
+        C.nPad = base;
+        C.nAcc = acc;
+        for (std::size_t gi = 0; gi < net.groups.size(); ++gi) {
+            const auto& g = net.groups[gi];
+            auto& Q = C.groups[gi];
+            Q.pre = g.pre;
+            Q.post = g.post;
+            Q.preOffset = g.preOffset;
+            Q.preCount = g.preCount;
+            Q.dense = g.dense ? 1 : 0;
+            Q.nPost = g.nPost;
+            Q.accBase = C.pops[g.post].acc[g.inhibitory ? 1 : 0];
+            Q.W = groupDev[gi].W;
+            Q.g = groupDev[gi].g;
+            Q.ind = groupDev[gi].ind;
+            Q.rowPtr = rowPtrDev[gi];
+        }
+        for (int b = 0; b < nSets; ++b) {
+            for (int pi = 0; pi < nPops; ++pi) C.pops[pi].P = pops[pi].kdev[b];
+            cycDev[b] = upload<ssbk::CycDev>(&C, 1);
+        }
+        allow_smem(reinterpret_cast<const void*>(&ssbk::cyclic_block_kernel), ssbk::kCycSmem);
     }
 
     // raster arena
@@ -1812,6 +1890,11 @@ void DeviceEngine::Impl::enqueue_windows(int W, int M) {
     auto after = [&](int sidx, cudaEvent_t e) {
         if (multi && e) CK(cudaStreamWaitEvent(S(sidx), e, 0));
     };
+    if (cycBlock) {
+        multiStream = false;
+        enqueue_cyclic(W, M);
+        return;
+    }
     if (multi) {
         cudaEvent_t fork = capture_event();
         CK(cudaEventRecord(fork, stream));
@@ -1858,6 +1941,63 @@ void DeviceEngine::Impl::enqueue_windows(int W, int M) {
             CK(cudaEventRecord(e, s));
             CK(cudaStreamWaitEvent(stream, e, 0));
         }
+}
+
+// Small recurrent networks (cycBlock): per window, the Poisson spikes and the
+// Izhikevich noise of the window (in the reference's stream order), the block
+// kernel over every population, then the raster -- one stream.
+void DeviceEngine::Impl::enqueue_cyclic(int W, int M) {
+    // the draws run one window ahead on a side stream (window-buffer sets
+    // keep them apart); the block kernel and the raster on the main stream
+    const bool multi = !cfg.profile && !serial && !auxStreams.empty();
+    cudaStream_t gs = multi ? auxStreams[0] : stream;
+    if (multi) {
+        cudaEvent_t fork = capture_event();
+        CK(cudaEventRecord(fork, stream));
+        CK(cudaStreamWaitEvent(gs, fork, 0));
+    }
+    std::vector<cudaEvent_t> done(M, nullptr);
+    for (int m = 0; m < M; ++m) {
+        const int b = m % nSets;
+        if (multi && m >= nSets) CK(cudaStreamWaitEvent(gs, done[m - nSets], 0));
+        launchStream = gs;
+        for (auto& P : pops) {
+            const ssbk::PopDev& K = P.kdev[b];
+            if (P.kind == kPoisson && P.n > 0) {
+                launch("poisson_window:" + P.name, [&] {
+                    const int bitsBytes = W * P.nwords * 4;
+                    const int inSmem = bitsBytes <= 32 * 1024;
+                    ssbk::poisson_window_kernel<<<1, 320, inSmem ? bitsBytes : 0, gs>>>(
+                        K, W, ssbk::kAccNone, ssbk::kAccNone, inSmem);
+                });
+            } else if (P.kind == kIzhikevich && P.n > 0) {
+                launch("gaussian_window:" + P.name, [&] {
+                    ssbk::gaussian_window_kernel<<<1, 320, 0, gs>>>(K, W);
+                });
+            }
+        }
+        if (multi) {
+            cudaEvent_t e = capture_event();
+            CK(cudaEventRecord(e, gs));
+            CK(cudaStreamWaitEvent(stream, e, 0));
+        }
+        launchStream = stream;
+        launch("cyclic_block", [&] {
+            ssbk::cyclic_block_kernel<<<1, ssbk::kCycThreads, ssbk::kCycSmem, stream>>>(cycDev[b], W);
+        });
+        launch("raster_window", [&] {
+            ssbk::raster_window_kernel<<<W * raster.nPops, 256, 0, stream>>>(rasterb[b], W);
+        });
+        if (multi) {
+            done[m] = capture_event();
+            CK(cudaEventRecord(done[m], stream));
+        }
+    }
+    if (multi) {
+        cudaEvent_t e = capture_event();
+        CK(cudaEventRecord(e, gs));
+        CK(cudaStreamWaitEvent(stream, e, 0));
+    }
 }
 
 // Switches the device to the other arena and drains the full one in the
