@@ -338,7 +338,6 @@ struct DeviceEngine::Impl {
     // small recurrent networks: one block runs each window (cyclic.cuh)
     bool cycBlock = false;
     ssbk::CycDev* cycDev[kMaxSets] = {};
-    std::vector<const long long*> rowPtrDev;  // CRS row pointers per group (device)
     int smCount = 148;
     // SMs the block-size choice leaves to the other populations' kernels,
     // which run concurrently in the window graphs (~10% with several
@@ -940,8 +939,12 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             }
         }
         for (const auto& g : net.groups) {
-            rows += g.preCount;
-            ok = ok && !g.rowSplit && g.preCount < (1 << 24);
+            rows = std::max(rows, g.preCount);
+            ok = ok && !g.rowSplit;
+            // the block expands CRS rows to dense ones: each post at most once per row
+            for (int r = 0; ok && !g.dense && r < g.preCount; ++r)
+                for (std::int64_t k = g.rowStart[r] + 1; k < g.rowStart[r + 1]; ++k)
+                    ok = ok && g.ind[k] > g.ind[k - 1];
         }
         cycBlock = ok && pad <= ssbk::kCycMaxN && nAcc <= ssbk::kCycMaxAcc && rows <= ssbk::kCycMaxRows;
     }
@@ -1225,7 +1228,6 @@ void DeviceEngine::Impl::build(const HostNet& net) {
 
     // groups
     groupDev.resize(net.groups.size());
-    rowPtrDev.assign(net.groups.size(), nullptr);
     for (std::size_t gi = 0; gi < net.groups.size(); ++gi) {
         const auto& g = net.groups[gi];
         auto& G = groupDev[gi];
@@ -1275,7 +1277,6 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             G.fullRows = g.nnz == static_cast<std::int64_t>(g.preCount) * g.nPost ? 1 : 0;
             long long* rs = upload<long long>(
                 reinterpret_cast<const long long*>(g.rowStart), static_cast<std::size_t>(g.nPre) + 1);
-            rowPtrDev[gi] = rs;
             int* seg = alloc<int>(static_cast<std::size_t>(g.preCount) * (G.nTiles + 1));
             const long long total = static_cast<long long>(g.preCount) * (G.nTiles + 1);
             if (total > 0) {
@@ -1452,13 +1453,18 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             Q.post = g.post;
             Q.preOffset = g.preOffset;
             Q.preCount = g.preCount;
-            Q.dense = g.dense ? 1 : 0;
             Q.nPost = g.nPost;
             Q.accBase = C.pops[g.post].acc[g.inhibitory ? 1 : 0];
             Q.W = groupDev[gi].W;
-            Q.g = groupDev[gi].g;
-            Q.ind = groupDev[gi].ind;
-            Q.rowPtr = rowPtrDev[gi];
+            if (!g.dense) {
+                // CRS as dense rows (absent entries +0.0f): the post-by-post
+                // fold over the spiking rows (the block bounds the size)
+                std::vector<float> dw(static_cast<std::size_t>(g.preCount) * g.nPost, 0.f);
+                for (int r = 0; r < g.preCount; ++r)
+                    for (std::int64_t k = g.rowStart[r]; k < g.rowStart[r + 1]; ++k)
+                        dw[static_cast<std::size_t>(r) * g.nPost + g.ind[k]] = g.g[k];
+                Q.W = upload<float>(dw.data(), dw.size());
+            }
         }
         for (int b = 0; b < nSets; ++b) {
             for (int pi = 0; pi < nPops; ++pi) C.pops[pi].P = pops[pi].kdev[b];

@@ -640,3 +640,26 @@ def test_storage_mode_auto_matches_reference_modes(oracle_mod, frac):
     assert_state_equal(g, o, spec, f"auto {frac}")
     dense_pn_kc = g.group_dense("pn_kc") is not None
     assert dense_pn_kc == (frac >= S.auto_dense_threshold())
+
+
+@pytest.mark.parametrize("window", [16, 256])
+@pytest.mark.parametrize("which", ["lif", "izh"])
+def test_cyclic_block_stepwise_state_matches_oracle(oracle_mod, which, window):
+    """Small recurrent networks run one block per window (cyclic.cuh): every
+    state array after irregular call sizes equals the oracle, and the block
+    kernel is the path that ran."""
+    spec = specs.recurrent_lif_spec(200, 200.0) if which == "lif" else specs.izh_spec(300, 30, 400.0)
+    g = gpu_sim(spec, window=window)
+    o = cpu_sim(oracle_mod, spec)
+    for n in [1, 2, 3, 5, 8, 13, 21, 34, 55, 89, 100]:
+        g.step(n)
+        o.step(n)
+        assert_state_equal(g, o, spec, f"after {o.steps_done()} steps")
+    rg, ro = g.finish(), o.finish()
+    assert np.array_equal(rg.raster.step, ro[0]) and np.array_equal(rg.raster.neuron, ro[2])
+    p = gpu_sim(spec, window=window, profile=True)
+    p.step(64)
+    p.sync()
+    names = {name for name, _, _ in p.kernel_stats()}
+    assert "cyclic_block" in names, names
+    p.close()
