@@ -904,7 +904,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         const std::size_t xdBytes = static_cast<std::size_t>(cfg.window) * g.nPre * 4;
         bool ok = net.pops[p].kind == kCondLif && g.pre != p && g.nPost <= ssbk::kTailMaxPost &&
                   net.pops[p].nGlobal == 0 && cfg.window <= ssbk::kSinkMaxW && xdBytes <= freeB / 4 &&
-                  ssbk::kSinkRing * ((net.pops[g.pre].n + 31) / 32) * 4 <= 160 * 1024 &&
+                  ssbk::kSinkRing * ((net.pops[g.pre].n + 31) / 32) * 4 + ssbk::kSinkLearnBytes <= 180 * 1024 &&
                   tailOf[p] < 0;
         for (const auto& h : net.groups) {
             if (h.pre == p) ok = false;                // a sink
@@ -1379,7 +1379,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             ssbk::TailDev T{};
             T.nSink = (g.nPost + ssbk::kSinkCols - 1) / ssbk::kSinkCols;
             // dynamic shared memory: the ring of L + 2 steps' pre spike bits
-            L.tailSmem = ssbk::kSinkRing * pops[g.pre].nwords * 4;
+            L.tailSmem = (ssbk::kSinkRing * pops[g.pre].nwords + 3) / 4 * 16 + ssbk::kSinkLearnBytes;
             allow_smem(reinterpret_cast<const void*>(&ssbk::sink_step_kernel), L.tailSmem);
             int perSm = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, ssbk::sink_step_kernel,
@@ -1412,7 +1412,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             T.decMinus = g.decMinus;
             T.wMax = g.wMax;
             if (const char* e = std::getenv("SSB_TAIL_SKIP")) T.skip = std::atoi(e);
-            T.fetchRound = 1;
+            T.fetchRound = 0;
             if (const char* e = std::getenv("SSB_SINK_FETCH")) T.fetchRound = std::atoi(e);
             for (int b = 0; b < nSets; ++b) {
                 L.tdev[b] = T;

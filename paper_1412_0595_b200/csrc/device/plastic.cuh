@@ -202,31 +202,9 @@ __device__ __forceinline__ void ring_load(const TailDev& T, uint32_t* ring, int 
     }
 }
 
-// The ring's share of a step's bits in four parts; part p: words
-// [p·part, (p + 1)·part), thread i takes p·part + i + k·kSinkRows
-constexpr int kRingPer = 5;  // words per thread and part (preWords <= 4·5·384)
-
-__device__ __forceinline__ void ring_fetch(const TailDev& T, int step, int i, int p, uint32_t* rv) {
-    const int part = (T.preWords + 3) / 4;
-    const int lo = p * part, hi = min(T.preWords, lo + part);
-    const uint32_t* pb = T.preBits + (size_t)step * T.preWords;
-#pragma unroll
-    for (int u = 0; u < kRingPer; ++u) {
-        const int k = lo + i + u * kSinkRows;
-        rv[u] = k < hi ? __ldg(pb + k) : 0u;
-    }
-}
-
-__device__ __forceinline__ void ring_store(const TailDev& T, uint32_t* ring, int step, int i, int p,
-                                           const uint32_t* rv) {
-    const int part = (T.preWords + 3) / 4;
-    const int lo = p * part, hi = min(T.preWords, lo + part);
-    uint32_t* dst = ring + (step % kSinkRing) * T.preWords;
-#pragma unroll
-    for (int u = 0; u < kRingPer; ++u) {
-        const int k = lo + i + u * kSinkRows;
-        if (k < hi) dst[k] = rv[u];
-    }
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src)
+                 : "memory");
 }
 
 // A producer thread's spiking row of a step: its index, its spike bits over
@@ -280,18 +258,12 @@ __device__ __forceinline__ void sink_fetch_all(const TailDev& T, int w, int e0, 
         out[k] = e0 + k * rows < cnt ? sink_fetch_row(T, w, rg[k], ring) : SinkRow{};
 }
 
-// Stage a spiking row's values for the fold -- after the potentiations it
-// owes (steps w - run .. w - 1, silent, where a column spiked: s_hist[s],
-// oldest first; xd(s + 1) = xd(s)·decPlus along a silent run, as the
-// prepass computes it) -- and store its learning at w (depression, +
-// potentiation where the column spiked at w).
-__device__ __forceinline__ void sink_row(const TailDev& T, int w, const SinkRow& q, const float* vals,
-                                         int c0, int nc, uint32_t spk, const float* s_yd,
-                                         const uint32_t* s_hist, float* stage) {
-    // stage[j * kSinkRows]: column j's slot of this row
-    float v[kSinkCols];
-#pragma unroll
-    for (int j = 0; j < kSinkCols; ++j) v[j] = vals[j];
+// A spiking row's values for the fold: its weights after the potentiations
+// it owes (steps w - run .. w - 1, silent, where a column spiked: s_hist[s],
+// oldest first; xd(s + 1) = xd(s)·decPlus along a silent run, as the prepass
+// computes it); xdw = xd(w).
+__device__ __forceinline__ void sink_stage(const TailDev& T, int w, const SinkRow& q, float* v,
+                                           const uint32_t* s_hist, float& xdw) {
     float xd = q.xs;
     for (int s = w - sink_run(q.hist, w); s < w; ++s) {
         const uint32_t m = s_hist[s];
@@ -300,29 +272,42 @@ __device__ __forceinline__ void sink_row(const TailDev& T, int w, const SinkRow&
             if ((m >> j) & 1u) v[j] = stdp_pot(v[j], xd, T.aPlus, T.wMax);
         xd = __fmul_rn(xd, T.decPlus);
     }
+    xdw = xd;
+}
+
+// The row's learning at w: depression, + potentiation where the column spiked.
+__device__ __forceinline__ void sink_learn(const TailDev& T, const SinkRow& q, const float* v,
+                                           float xdw, int c0, int nc, uint32_t spk, const float* yd,
+                                           float* out) {
 #pragma unroll
     for (int j = 0; j < kSinkCols; ++j) {
-        stage[j * kSinkRows] = v[j];
+        out[j] = 0.f;
         if (j >= nc) continue;
-        float nv = __fsub_rn(v[j], __fmul_rn(T.aMinus, s_yd[j]));
-        if ((spk >> j) & 1u) nv = __fadd_rn(nv, __fmul_rn(T.aPlus, xd));
-        T.WT[(size_t)(c0 + j) * T.nPre + q.r] = stdp_clip(nv, T.wMax);
+        float nv = __fsub_rn(v[j], __fmul_rn(T.aMinus, yd[j]));
+        if ((spk >> j) & 1u) nv = __fadd_rn(nv, __fmul_rn(T.aPlus, xdw));
+        out[j] = stdp_clip(nv, T.wMax);
+        T.WT[(size_t)(c0 + j) * T.nPre + q.r] = out[j];
     }
 }
 
-constexpr int kSinkPre = 4;  // chunks of a step whose rows are fetched ahead
-static_assert(kSinkPre == 4, "ring_fetch splits a step's bits in four parts");
+constexpr int kSinkPre = 4;    // chunks of a step whose rows are fetched ahead
+constexpr int kSinkBufs = 8;   // staged chunk buffers (a ring between producers and the chains)
+constexpr int kSinkProdWarps = kSinkRows / 32;
+constexpr int kSinkLearnBytes = 2 * kSinkCols * kSinkPre * kSinkRows * 4;
 
 __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, int W) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
-    __shared__ __align__(16) float s_stage[2][kSinkCols][kSinkRows];  // a column's rows contiguous
-    __shared__ float s_yd[kSinkCols];
+    __shared__ __align__(16) float s_stage[kSinkBufs][kSinkCols][kSinkRows];  // a column's rows contiguous
+    __shared__ __align__(8) uint64_t s_full[kSinkBufs], s_empty[kSinkBufs], s_dn[2], s_pdone[2];
+    __shared__ float s_yd[2][kSinkCols];
     __shared__ uint32_t s_hist[kSinkMaxW];  // sink: the block's column spikes of each step
-    __shared__ int s_cnt;
+    __shared__ int s_idx[3][kSinkPre][kSinkRows];  // producers: step w's rows at w % 3 (global index), ascending
     __shared__ long long s_red[32];
-    __shared__ unsigned long long s_tw;
-    extern __shared__ uint32_t s_bitRing[];  // sink: pre spike bits [L + 1][preWords]
+    extern __shared__ __align__(16) uint32_t s_bitRing[];  // sink: pre spike bits [L + 2][preWords],
+    // then the rows' learned weights [2][kSinkCols][kSinkPre * kSinkRows] (producers)
+    using LearnBuf = float[kSinkCols][kSinkPre * kSinkRows];
+    LearnBuf* s_learn = reinterpret_cast<LearnBuf*>(s_bitRing + ((kSinkRing * T.preWords + 3) & ~3));
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const PopDev& P = T.P;
     const int nPre = T.nPre;
@@ -332,6 +317,17 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
         for (int i = t; i < W; i += blockDim.x) T.sinkDone[i] = T.bgDone[i] = 0;
     }
     const bool sink = static_cast<int>(blockIdx.x) < T.nSink;
+    if (sink && t == 0) {
+        for (int b = 0; b < kSinkBufs; ++b) {
+            mbar_init(&s_full[b], kSinkProdWarps);
+            mbar_init(&s_empty[b], 1);
+        }
+        mbar_init(&s_dn[0], 1);
+        mbar_init(&s_dn[1], 1);
+        mbar_init(&s_pdone[0], kSinkProdWarps);
+        mbar_init(&s_pdone[1], kSinkProdWarps);
+        mbar_fence_init();
+    }
     grid.sync();
     if (!sink) {
         sink_background(T, W, reinterpret_cast<uint32_t*>(s_hist));
@@ -340,87 +336,64 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
     const int c0 = blockIdx.x * kSinkCols;
     const int nc = min(kSinkCols, T.nPost - c0);
     const bool col = warp == 0 && lane < nc;
-    const LifConst lc = lif_const(P);
-    float v = 0.f, ge = 0.f, gi = 0.f, y = 0.f, a = 0.f;
-    uint32_t flag = 1, expMax = 0, bad = 0;
-    if (col) {
-        v = P.v[c0 + lane];
-        ge = P.gExc[c0 + lane];
-        gi = P.gInh[c0 + lane];
-        flag = P.nanFlag[c0 + lane] ? 1u : 0u;
-        y = T.y[c0 + lane];
-    }
+    // producers: the warps off scheduler 0, where warp 0 (post update + the
+    // column chains, the step's critical path) issues alone
     const bool producer = (warp & 3) != 0;
     const int i = ((warp >> 2) * 3 + (warp & 3) - 1) * 32 + lane;  // producers: chunk row i
-    SinkRow rec[kSinkPre], recN[kSinkPre];
-    int nextCnt = 0, pendK = -1, idxN = -1;
-    uint32_t rv[kRingPer];
-    if (producer && W > 0) {
-        const int cn = T.skip & 1 ? 0 : T.preCnt[0];
-        sink_fetch_all<kSinkPre>(T, 0, i, kSinkRows, cn, s_bitRing, rec);
-        ring_load(T, s_bitRing, 0, i, kSinkRows);
-    }
-    // SSB_TRACE: block 0 records each step: {tag | count << 32, post update end
-    // | rows end << 32 (ns from the step's start), 0, chain cycles}
+    // SSB_TRACE: warp 0 of block 0 records each step: {tag | count << 32,
+    // post update end (ns from the step's start) | chains end << 32, 0, chain cycles}
     const bool tr = g_trace != nullptr && t == 0 && blockIdx.x == 0;
     unsigned trBase = 0;
-    if (tr) trBase = atomicAdd(&g_traceN, static_cast<unsigned>(2 * W));
-    for (int w = 0; w < W; ++w) {
-        unsigned long long t0 = 0, tA = 0, tR[4] = {0, 0, 0, 0};
-        long long chainCy = 0;
-        if (tr) {
-            t0 = global_ns();
-            s_tw = t0;
+    if (tr) trBase = atomicAdd(&g_traceN, static_cast<unsigned>(W));
+    if (warp == 0) {
+        // ---- the post neurons and the column chains
+        const LifConst lc = lif_const(P);
+        float v = 0.f, ge = 0.f, gi = 0.f, y = 0.f, a = 0.f;
+        uint32_t flag = 1, expMax = 0, bad = 0;
+        if (col) {
+            v = P.v[c0 + lane];
+            ge = P.gExc[c0 + lane];
+            gi = P.gInh[c0 + lane];
+            flag = P.nanFlag[c0 + lane] ? 1u : 0u;
+            y = T.y[c0 + lane];
         }
-        float wv[kSinkPre][kSinkCols];
-        if (warp == 0) {
+        int g = 0;  // chunk sequence number (the producers count the same way)
+        int cntNext = W > 0 && !(T.skip & 1) ? T.preCnt[0] : 0;
+        for (int w = 0; w < W; ++w) {
+            unsigned long long t0 = 0, tA = 0, waitNs = 0;
+            long long chainCy = 0;
+            if (tr) t0 = global_ns();
+            const int cnt = cntNext;
+            cntNext = w + 1 < W && !(T.skip & 1) ? __ldg(T.preCnt + w + 1) : 0;
+            // the producers have read step w - 2's post spikes and traces
+            // (their slots are rewritten now; steps without spikes need no
+            // producer, so warp 0 could otherwise run ahead)
+            if (w >= 2) mbar_wait(&s_pdone[w & 1], ((w - 2) >> 1) & 1);
             const float ex = w == 0 ? (col ? P.excIn[c0 + lane] : 0.f) : a;
             const float ih = w == 0 ? (col ? P.inhIn[c0 + lane] : 0.f) : 0.f;
             bool spike = false;
             if (col) spike = lif_step<true>(lc, ex, ih, v, ge, gi, expMax, bad);
             const uint32_t m = __ballot_sync(kFull, spike);
             if (spike) atomicOr(P.bits + (size_t)w * P.nwords + ((c0 + lane) >> 5), 1u << ((c0 + lane) & 31));
-            if (lane == 0) {
-                s_hist[w] = m;
-                s_cnt = T.skip & 1 ? 0 : T.preCnt[w];
-            }
             const float yd = __fmul_rn(y, T.decMinus);
-            if (lane < kSinkCols) s_yd[lane] = yd;
+            if (lane < kSinkCols) s_yd[w & 1][lane] = yd;
+            if (lane == 0) s_hist[w] = m;
             y = spike ? __fadd_rn(yd, 1.0f) : yd;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_dn[w & 1]);
+            if (tr) tA = global_ns();
+            // the fold of step w: the staged chunks in order, rows ascending
             a = 0.f;
-        } else if (producer) {
-            // the background's step w - L - 1 is in (rows spiking now may have
-            // been silent through it); then the fetched rows' weights
-            nextCnt = w + 1 < W && !(T.skip & 1) ? __ldg(T.preCnt + w + 1) : 0;
-            if (w > kSinkLag) {
-                if (t == 32) {
-                    spin_until(T.bgDone + (w - kSinkLag - 1), gridDim.x - T.nSink);
-                    if (g_trace) s_tw = global_ns();
-                }
-                asm volatile("bar.sync 1, %0;" ::"r"(kSinkRows));
-            }
-#pragma unroll
-            for (int kk = 0; kk < kSinkPre; ++kk)
-#pragma unroll
-                for (int j = 0; j < kSinkCols; ++j)
-                    wv[kk][j] = rec[kk].r >= 0 && j < nc
-                                    ? __ldcg(T.WT + (size_t)(c0 + j) * nPre + rec[kk].r) : 0.f;
-        }
-        __syncthreads();
-        if (t == 32) {  // the block's post spikes of w are out (off warp 0's path)
-            __threadfence();
-            atomicAdd(T.sinkDone + w, 1);
-        }
-        if (tr) tA = global_ns();
-        const uint32_t spk = s_hist[w];
-        const int cnt = s_cnt;
-        const int nChunks = (cnt + kSinkRows - 1) / kSinkRows;
-        for (int k = 0; k <= nChunks; ++k) {
-            if (warp == 0) {
-                if (k > 0 && lane < kSinkCols) {  // the column chains of chunk k - 1
+            const int nCh = (cnt + kSinkRows - 1) / kSinkRows;
+            for (int k = 0; k < nCh; ++k, ++g) {
+                const int b = g % kSinkBufs;
+                const unsigned long long tw0 = tr ? global_ns() : 0;
+                mbar_wait(&s_full[b], (g / kSinkBufs) & 1);
+                if (tr) waitNs += global_ns() - tw0;
+                if (lane < kSinkCols) {
                     const long long cy0 = tr ? clock64() : 0;
-                    const int n = min(kSinkRows, cnt - (k - 1) * kSinkRows);
-                    const float* sb = &s_stage[(k - 1) & 1][lane][0];
+                    const int n = min(kSinkRows, cnt - k * kSinkRows);
+                    const float* sb = &s_stage[b][lane][0];
                     // four staged values per 16-byte load, the next four loading
                     // while the current four add (the chain is the step's floor)
                     const int n4 = n & ~3;
@@ -446,92 +419,176 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
                         chainCy += clock64() - cy0;
                     }
                 }
-            } else if (producer) {
-                if (k < nChunks) {
-                    const int e = k * kSinkRows + i;
-                    float* stage = &s_stage[k & 1][0][i];
-                    if (k < kSinkPre) {
-#pragma unroll
-                        for (int kk = 0; kk < kSinkPre; ++kk)
-                            if (kk == k && e < cnt) {
-                                if (rec[kk].r >= 0)
-                                    sink_row(T, w, rec[kk], wv[kk], c0, nc, spk, s_yd, s_hist, stage);
-                                else
-                                    for (int j = 0; j < kSinkCols; ++j) stage[j * kSinkRows] = 0.f;
-                            }
-                    } else if (e < cnt) {  // beyond the fetched chunks: on demand
-                        const SinkRow q = sink_fetch(T, w, e, cnt, s_bitRing);
-                        if (q.r >= 0) {
-                            float vals[kSinkCols];
-#pragma unroll
-                            for (int j = 0; j < kSinkCols; ++j)
-                                vals[j] = j < nc ? __ldcg(T.WT + (size_t)(c0 + j) * nPre + q.r) : 0.f;
-                            sink_row(T, w, q, vals, c0, nc, spk, s_yd, s_hist, stage);
-                        } else {
-                            for (int j = 0; j < kSinkCols; ++j) stage[j * kSinkRows] = 0.f;
-                        }
-                    }
-                }
-                // in each round's slack (the chains are the longer part), a
-                // share of the next step's rows and pre spike bits (read-only):
-                // round k issues the loads of chunk k's row and ring part k,
-                // round k + 1 consumes them; the last round finishes the rest
-                if (w + 1 < W) {
-                    if (pendK >= 0) {
-#pragma unroll
-                        for (int kk = 0; kk < kSinkPre; ++kk)
-                            if (kk == pendK) recN[kk] = idxN >= 0 ? sink_fetch_row(T, w + 1, idxN, s_bitRing) : SinkRow{};
-                        ring_store(T, s_bitRing, w + 1, i, pendK, rv);
-                        pendK = -1;
-                    }
-                    if (k < nChunks && k < kSinkPre) {
-                        const int e = k * kSinkRows + i;
-                        idxN = e < nextCnt ? __ldg(T.preList + (size_t)(w + 1) * T.preN + e) : -1;
-                        ring_fetch(T, w + 1, i, k, rv);
-                        pendK = k;
-                    } else if (k == nChunks) {
-#pragma unroll
-                        for (int kk = 0; kk < kSinkPre; ++kk)
-                            if (kk >= k) {
-                                recN[kk] = sink_fetch(T, w + 1, kk * kSinkRows + i, nextCnt, s_bitRing);
-                                ring_fetch(T, w + 1, i, kk, rv);
-                                ring_store(T, s_bitRing, w + 1, i, kk, rv);
-                            }
-                    }
-                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_empty[b]);
             }
-            // the last round needs no barrier: warp 0 goes on to the next
-            // post update, the producers to the next step's weights, and the
-            // step's first barrier joins them before any chunk is restaged
-            if (k < nChunks) __syncthreads();
-            if (tr && k < 4) tR[k] = global_ns() - t0;
+            if (tr && trBase + w < g_traceCap) {
+                unsigned long long* e = g_trace + 4ull * (trBase + w);
+                e[0] = 0x5100ull | (static_cast<unsigned long long>(cnt) << 32);
+                e[1] = (tA - t0) | ((global_ns() - t0) << 32);
+                e[2] = waitNs;  // warp 0 waiting for staged chunks
+                e[3] = static_cast<unsigned long long>(chainCy);
+            }
+        }
+        // ---- end of window: post state, next window's first input, traces
+        if (col) {
+            const int j = c0 + lane;
+            P.v[j] = v;
+            P.gExc[j] = ge;
+            P.gInh[j] = gi;
+            P.excIn[j] = a;
+            P.inhIn[j] = 0.f;
+            P.nanFlag[j] = static_cast<uint8_t>(flag | (expMax == 0x7f800000u));
+            T.y[j] = y;
+            if (!flag && expMax == 0x7f800000u) atomicAdd(P.flagged, 1ull);
+        }
+        (void)s_red;
+        return;
+    }
+    if (!producer) return;
+    // ---- producers: stage each step's rows (a step ahead of the chains),
+    //      then, once the step's post spikes are out, its learning.  A step's
+    //      weights load during the step before (only rows that spiked at that
+    //      step change in between: their learned values come from s_learn).
+    SinkRow rec[kSinkPre], recN[kSinkPre];
+    float v[kSinkPre][kSinkCols], vN[kSinkPre][kSinkCols];
+    int cntCur = W > 0 && !(T.skip & 1) ? T.preCnt[0] : 0;
+    if (W > 0) {
+        sink_fetch_all<kSinkPre>(T, 0, i, kSinkRows, cntCur, s_bitRing, rec);
+#pragma unroll
+        for (int kk = 0; kk < kSinkPre; ++kk) {
+            s_idx[0][kk][i] = rec[kk].r >= 0 ? rec[kk].r + T.preOffset : INT_MAX;
+#pragma unroll
+            for (int j = 0; j < kSinkCols; ++j)
+                v[kk][j] = rec[kk].r >= 0 && j < nc ? __ldcg(T.WT + (size_t)(c0 + j) * nPre + rec[kk].r) : 0.f;
+        }
+        ring_load(T, s_bitRing, 0, i, kSinkRows);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(kSinkRows));
+    int g = 0, cntPrev = 0;
+    for (int w = 0; w < W; ++w) {
+        const int cnt = cntCur;
+        const int nCh = (cnt + kSinkRows - 1) / kSinkRows;
+        const int nextCnt = w + 1 < W && !(T.skip & 1) ? __ldg(T.preCnt + w + 1) : 0;
+        // rows that spiked at w - 1 too: their weights after that step's learning
+        if (w > 0) {
+            const int* prevIdx = &s_idx[(w - 1) % 3][0][0];  // step w - 1's rows, ascending
+            const int nPrev = min(cntPrev, kSinkPre * kSinkRows);
+#pragma unroll
+            for (int kk = 0; kk < kSinkPre; ++kk) {
+                if (rec[kk].r < 0 || !(rec[kk].hist & 1u)) continue;
+                const int key = rec[kk].r + T.preOffset;
+                int lo = 0, hi = nPrev;  // first position with prevIdx >= key
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (prevIdx[mid] < key) lo = mid + 1;
+                    else hi = mid;
+                }
+#pragma unroll
+                for (int j = 0; j < kSinkCols; ++j)
+                    v[kk][j] = j >= nc ? 0.f
+                               : lo < nPrev && prevIdx[lo] == key
+                                   ? s_learn[(w - 1) & 1][j][lo]
+                                   : __ldcg(T.WT + (size_t)(c0 + j) * nPre + rec[kk].r);  // on-demand row
+            }
+        }
+        // stage the fetched chunks (s_hist of the steps before w is final: the
+        // producers waited for the post update of w - 1)
+        float xdw[kSinkPre];
+#pragma unroll
+        for (int kk = 0; kk < kSinkPre; ++kk) {
+            if (kk >= nCh) break;
+            const int gg = g + kk, b = gg % kSinkBufs;
+            xdw[kk] = 0.f;
+            if (rec[kk].r >= 0) sink_stage(T, w, rec[kk], v[kk], s_hist, xdw[kk]);
+            if (gg >= kSinkBufs) mbar_wait(&s_empty[b], ((gg / kSinkBufs) - 1) & 1);
+            const bool live = kk * kSinkRows + i < cnt;
+#pragma unroll
+            for (int j = 0; j < kSinkCols; ++j) s_stage[b][j][i] = live && rec[kk].r >= 0 ? v[kk][j] : 0.f;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_full[b]);
+        }
+        // the next step's row indices and pre spike bits, copied asynchronously
+        if (w + 1 < W) {
+            const int* Ln = T.preList + (size_t)(w + 1) * T.preN;
+#pragma unroll
+            for (int kk = 0; kk < kSinkPre; ++kk) {
+                if (kk * kSinkRows + i < nextCnt) cp_async4(&s_idx[(w + 1) % 3][kk][i], Ln + kk * kSinkRows + i);
+                else s_idx[(w + 1) % 3][kk][i] = INT_MAX;
+            }
+            const uint32_t* pb = T.preBits + (size_t)(w + 1) * T.preWords;
+            uint32_t* dst = s_bitRing + ((w + 1) % kSinkRing) * T.preWords;
+            for (int k = i; k < T.preWords; k += kSinkRows) cp_async4(dst + k, pb + k);
+            cp_async_commit();
+        }
+        // the step's post spikes, then its learning
+        mbar_wait(&s_dn[w & 1], (w >> 1) & 1);
+        const uint32_t spk = s_hist[w];
+        const float yd[kSinkCols] = {s_yd[w & 1][0], s_yd[w & 1][1]};
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_pdone[w & 1]);
+        if (t == 32) {  // the block's post spikes of w are out
+            __threadfence();
+            atomicAdd(T.sinkDone + w, 1);
         }
 #pragma unroll
-        for (int kk = 0; kk < kSinkPre; ++kk) rec[kk] = recN[kk];
-        if (tr && trBase + 2 * w + 1 < g_traceCap) {
-            unsigned long long* e = g_trace + 4ull * (trBase + 2 * w);
-            e[0] = 0x5100ull | (static_cast<unsigned long long>(cnt) << 32);
-            e[1] = (tA - t0) | ((global_ns() - t0) << 32);
-            e[2] = s_tw - t0;
-            e[3] = static_cast<unsigned long long>(chainCy);
-            e[4] = 0x5101ull;
-            e[5] = tR[0] | (tR[1] << 32);
-            e[6] = tR[2];
-            e[7] = tR[3];
+        for (int kk = 0; kk < kSinkPre; ++kk) {
+            if (kk >= nCh || kk * kSinkRows + i >= cnt || rec[kk].r < 0) continue;
+            float lw[kSinkCols];
+            sink_learn(T, rec[kk], v[kk], xdw[kk], c0, nc, spk, yd, lw);
+#pragma unroll
+            for (int j = 0; j < kSinkCols; ++j) s_learn[w & 1][j][kk * kSinkRows + i] = lw[j];
         }
+        for (int k = kSinkPre; k < nCh; ++k) {  // beyond the fetched chunks: on demand
+            const int gg = g + k, b = gg % kSinkBufs;
+            const int e = k * kSinkRows + i;
+            const SinkRow q = sink_fetch(T, w, e, cnt, s_bitRing);
+            float vv[kSinkCols] = {0.f, 0.f};
+            float xw = 0.f;
+            if (q.r >= 0) {
+#pragma unroll
+                for (int j = 0; j < kSinkCols; ++j)
+                    vv[j] = j < nc ? __ldcg(T.WT + (size_t)(c0 + j) * nPre + q.r) : 0.f;
+                sink_stage(T, w, q, vv, s_hist, xw);
+            }
+            if (gg >= kSinkBufs) mbar_wait(&s_empty[b], ((gg / kSinkBufs) - 1) & 1);
+#pragma unroll
+            for (int j = 0; j < kSinkCols; ++j) s_stage[b][j][i] = q.r >= 0 ? vv[j] : 0.f;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_full[b]);
+            float lw[kSinkCols];
+            if (q.r >= 0) sink_learn(T, q, vv, xw, c0, nc, spk, yd, lw);
+        }
+        g += nCh;
+        if (w + 1 < W) {
+            // the next step's rows from the copies issued above, and their
+            // weights: final except for the rows spiking now (fixed up above
+            // from s_learn) once the background's step w - L is in
+            cp_async_wait<0>();
+#pragma unroll
+            for (int kk = 0; kk < kSinkPre; ++kk) {
+                const int e = kk * kSinkRows + i;
+                recN[kk] = e < nextCnt ? sink_fetch_row(T, w + 1, s_idx[(w + 1) % 3][kk][i], s_bitRing)
+                                       : SinkRow{};
+            }
+            if (w + 1 > kSinkLag) spin_until(T.bgDone + (w - kSinkLag), gridDim.x - T.nSink);
+#pragma unroll
+            for (int kk = 0; kk < kSinkPre; ++kk)
+#pragma unroll
+                for (int j = 0; j < kSinkCols; ++j)
+                    vN[kk][j] = recN[kk].r >= 0 && j < nc
+                                    ? __ldcg(T.WT + (size_t)(c0 + j) * nPre + recN[kk].r) : 0.f;
+        }
+        cntPrev = cnt;
+        cntCur = nextCnt;
+#pragma unroll
+        for (int kk = 0; kk < kSinkPre; ++kk) {
+            rec[kk] = recN[kk];
+#pragma unroll
+            for (int j = 0; j < kSinkCols; ++j) v[kk][j] = vN[kk][j];
+        }
+        // every producer's learning of w (s_learn, the weights) and ring slot
+        // w + 1 in before step w + 1 is staged
+        asm volatile("bar.sync 1, %0;" ::"r"(kSinkRows));
     }
-    // ---- end of window: post state, next window's first input, traces
-    if (col) {
-        const int j = c0 + lane;
-        P.v[j] = v;
-        P.gExc[j] = ge;
-        P.gInh[j] = gi;
-        P.excIn[j] = a;
-        P.inhIn[j] = 0.f;
-        P.nanFlag[j] = static_cast<uint8_t>(flag | (expMax == 0x7f800000u));
-        T.y[j] = y;
-    }
-    const int newly = col && !flag && expMax == 0x7f800000u ? 1 : 0;
-    const long long tot = block_sum(static_cast<long long>(newly), s_red);
-    if (t == 0 && tot) atomicAdd(P.flagged, (unsigned long long)tot);
 }

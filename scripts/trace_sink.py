@@ -43,7 +43,7 @@ s = tag == 0x5100
 print("steps", int(s.sum()), "spiking rows per step", cnt[s].mean())
 stat("step (sink block 0)", tB[s])
 stat("sink post update", tA[s])
-stat("  background wait end", tS[s])
+stat("  chains waiting for staged chunks", rec[s, 2].astype(np.float64) / 1e3)
 stat("sink rows", tB[s] - tA[s])
 print(f"chain: {cy[s].sum() / cnt[s].sum():.2f} cycles per row")
 r = tag == 0x5101
