@@ -903,7 +903,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         CK(cudaMemGetInfo(&freeB, &totalB));
         const std::size_t xdBytes = static_cast<std::size_t>(cfg.window) * g.nPre * 4;
         bool ok = net.pops[p].kind == kCondLif && g.pre != p && g.nPost <= ssbk::kTailMaxPost &&
-                  net.pops[p].nGlobal == 0 && cfg.window <= ssbk::kSinkMaxW && xdBytes <= freeB / 4 &&
+                  net.pops[p].nGlobal == 0 && net.pops[g.pre].nGlobal == 0 && !g.rowSplit &&
+                  cfg.window <= ssbk::kSinkMaxW && xdBytes <= freeB / 4 &&
                   ssbk::kSinkRing * ((net.pops[g.pre].n + 31) / 32) * 4 + ssbk::kSinkLearnBytes <= 180 * 1024 &&
                   tailOf[p] < 0;
         for (const auto& h : net.groups) {
