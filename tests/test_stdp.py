@@ -139,3 +139,34 @@ def test_gpu_stdp_rejects_split_worlds():
     spec = specs.stdp_mbody_spec(1000, 10.0)
     with pytest.raises(S.SpecError):
         S.Simulation(spec, S.StorageMode.FromSpec, S.EngineOptions(virtualWorld=2))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("window", [64, 256])
+def test_gpu_plastic_sink_matches_step_mode_config3(monkeypatch, window):
+    """Config 3 + STDP over 0.3 s (DN volleys, the background's lag, many
+    windows): the windowed plastic-sink path and step mode give the same
+    weights, rasters and state, bit for bit."""
+    spec = specs.stdp_mbody_spec(100_000, 300.0)
+    runs = []
+    for tail in ("1", "0"):
+        monkeypatch.setenv("SSB_PLASTIC_TAIL", tail)
+        sim = S.Simulation(spec, S.StorageMode.FromSpec, S.EngineOptions(window=window))
+        sim.step(1234)
+        w_mid = sim.group_weights("kc_dn").copy()
+        sim.step(1766)
+        w_end = sim.group_weights("kc_dn").copy()
+        state = {(pi, f): sim.pull(pi, f) for pi, p in enumerate(spec.populations)
+                 if p.model != S.ModelKind.PoissonSource for f in ("v", "gExc", "gInh", "excIn")}
+        r = sim.finish()
+        runs.append((w_mid, w_end, r, state))
+        sim.close()
+    (wa, wb, ra, sa), (wc, wd, rc, sc) = runs
+    assert np.array_equal(wa, wc) and np.array_equal(wb, wd)
+    assert np.array_equal(ra.raster.step, rc.raster.step)
+    assert np.array_equal(ra.raster.neuron, rc.raster.neuron)
+    assert np.array_equal(ra.raster.population, rc.raster.population)
+    dn = [p.name for p in spec.populations].index("dn")
+    assert int((ra.raster.population == dn).sum()) > 1000  # volleys happened
+    for k in sa:
+        assert specs.bits_equal(sa[k], sc[k]), k
