@@ -1,0 +1,6 @@
+# round-end evidence: GPU suite, full bench line (default flags), launch list
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1
+tail -3 gpurun_out/gputest.log
+python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
+tail -c 600 gpurun_out/bench_final.json
