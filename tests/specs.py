@@ -174,10 +174,11 @@ def hh_mbody_spec(n_kc: int = 300, duration_ms: float = 30.0, seed: int = 7) -> 
 
 
 def stdp_mbody_spec(n_kc: int, duration_ms: float, frac: float = 0.05, seed: int = 7,
-                    a_plus: float = 0.1, a_minus: float = 0.12, w_max: float = 3.0):
+                    a_plus: float = 0.1, a_minus: float = 0.12, w_max: float = 3.0,
+                    n_dn: int = 100):
     """Extension F2: the mushroom body with STDP on kc_dn (amplitudes and wMax
     relative to the built kc_dn weight)."""
-    spec = mbody_spec(n_kc, frac, duration_ms, seed=seed)
+    spec = mbody_spec(n_kc, frac, duration_ms, seed=seed, n_dn=n_dn)
     g = spec.synapses[spec.group_index("kc_dn")]
     w0 = g.baseWeight.value * g.gScale
     g.stdp = S.StdpRule(aPlus=a_plus * w0, aMinus=a_minus * w0, tauPlusMs=20.0,

@@ -170,3 +170,31 @@ def test_gpu_plastic_sink_matches_step_mode_config3(monkeypatch, window):
     assert int((ra.raster.population == dn).sum()) > 1000  # volleys happened
     for k in sa:
         assert specs.bits_equal(sa[k], sc[k]), k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_kc, n_dn", [(1003, 37), (4099, 65), (20000, 128)])
+def test_gpu_plastic_sink_odd_sizes_match_oracle(oracle_mod, n_kc, n_dn):
+    """Ragged shapes of the plastic-sink path: a partial column block, pre rows
+    not a multiple of four (the scalar background path), the largest sink;
+    weights, raster and state equal the oracle's."""
+    spec = specs.stdp_mbody_spec(n_kc, 200.0, n_dn=n_dn, a_plus=0.3)
+    gi = spec.group_index("kc_dn")
+    g = S.Simulation(spec, S.StorageMode.FromSpec, S.EngineOptions(window=64))
+    o = cpu_sim(oracle_mod, spec)
+    g.step(g.steps_total())
+    o.step(o.steps_total())
+    assert np.array_equal(g.group_weights("kc_dn"), o.group(gi)[1])
+    r, ro = g.finish(), o.finish()
+    assert np.array_equal(r.raster.step, ro[0]) and np.array_equal(r.raster.neuron, ro[2])
+    assert np.array_equal(r.raster.population, ro[1])
+    for pi, p in enumerate(spec.populations):
+        if p.model == S.ModelKind.PoissonSource:
+            continue
+        for f in ("v", "gExc", "gInh", "excIn"):
+            assert specs.bits_equal(g.pull(pi, f), o.state(pi, f)), f"{p.name}.{f}"
+    p = S.Simulation(spec, S.StorageMode.FromSpec, S.EngineOptions(window=64, profile=True))
+    p.step(128)
+    p.sync()
+    assert any(name.startswith("sink_step") for name, _, _ in p.kernel_stats())
+    p.close()
