@@ -1413,8 +1413,6 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             T.decMinus = g.decMinus;
             T.wMax = g.wMax;
             if (const char* e = std::getenv("SSB_TAIL_SKIP")) T.skip = std::atoi(e);
-            T.fetchRound = 0;
-            if (const char* e = std::getenv("SSB_SINK_FETCH")) T.fetchRound = std::atoi(e);
             for (int b = 0; b < nSets; ++b) {
                 L.tdev[b] = T;
                 L.tdev[b].P = Q.devb[b];

@@ -58,7 +58,6 @@ struct TailDev {
     int* bgDone;                // [Wmax]: background blocks done with step s
     int nPre, nPost, nSink;
     int skip;  // diagnostic (SSB_TAIL_SKIP, timing only): 1 no sink rows, 2 no background
-    int fetchRound;  // round of a step in which the next step's rows are fetched (SSB_SINK_FETCH)
     float aPlus, aMinus, decPlus, decMinus, wMax;
 };
 
