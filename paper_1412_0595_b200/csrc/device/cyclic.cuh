@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(kCycThreads, 1) cyclic_block_kernel(const CycD
         for (int i = t; i < nAcc; i += blockDim.x) s_acc[i] = 0.f;
         for (int gq = 0; gq < D.nGroups; ++gq) {
             const CycGroup& G = D.groups[gq];
+            if (G.accBase < 0) continue;  // into a Poisson population: no input to keep
             // the group's spiking pre rows, ascending (a barrier ends the scans)
             const int base = D.pops[G.pre].base + G.preOffset;
             int nRows = 0;
