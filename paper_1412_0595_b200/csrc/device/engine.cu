@@ -1413,6 +1413,25 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             T.decMinus = g.decMinus;
             T.wMax = g.wMax;
             if (const char* e = std::getenv("SSB_TAIL_SKIP")) T.skip = std::atoi(e);
+            if (std::getenv("SSB_SINK_WATCH")) {  // diagnostic: a thread prints each role's progress
+                int* hw = nullptr;
+                CK(cudaHostAlloc(&hw, 4 * (3 * T.nSink + 1) * sizeof(int), cudaHostAllocMapped));
+                int* dw = nullptr;
+                CK(cudaHostGetDevicePointer(&dw, hw, 0));
+                CK(cudaMemcpyToSymbol(ssbk::g_watch, &dw, sizeof(dw)));
+                const int ns = T.nSink;
+                std::thread([hw, ns] {
+                    for (;;) {
+                        std::this_thread::sleep_for(std::chrono::seconds(2));
+                        volatile int* v = hw;
+                        std::fprintf(stderr, "watch: bg %d | chains", v[3 * ns]);
+                        for (int b = 0; b < std::min(ns, 4); ++b) std::fprintf(stderr, " %d/%d", v[2 * b], v[2 * b + 1]);
+                        std::fprintf(stderr, " | producers");
+                        for (int b = 0; b < std::min(ns, 4); ++b) std::fprintf(stderr, " %d", v[2 * ns + b]);
+                        std::fprintf(stderr, "\n");
+                    }
+                }).detach();
+            }
             for (int b = 0; b < nSets; ++b) {
                 L.tdev[b] = T;
                 L.tdev[b].P = Q.devb[b];

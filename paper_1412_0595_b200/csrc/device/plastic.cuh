@@ -89,6 +89,8 @@ __device__ __forceinline__ uint32_t pre_word(const TailDev& T, int step, int i) 
     return __ldg(T.preBits + (size_t)step * T.preWords + (i >> 5));
 }
 
+__device__ int* g_watch = nullptr;  // diagnostic (SSB_SINK_WATCH): progress of each role
+
 __device__ __forceinline__ void spin_until(const int* ctr, int target) {
     while (*reinterpret_cast<const volatile int*>(ctr) < target) __nanosleep(32);
     __threadfence();
@@ -171,6 +173,7 @@ __device__ void sink_background(const TailDev& T, int W, uint32_t* s_m) {
         if (threadIdx.x == 0) {
             __threadfence();
             atomicAdd(T.bgDone + s, 1);
+            if (g_watch && static_cast<int>(blockIdx.x) == T.nSink) g_watch[3 * T.nSink] = s;
         }
     }
 }
@@ -289,20 +292,27 @@ __device__ __forceinline__ void sink_learn(const TailDev& T, const SinkRow& q, c
     }
 }
 
+struct SinkState {
+    float v, ge, gi, y;
+    uint32_t flag, expMax;
+};
+
 constexpr int kSinkPre = 4;    // chunks of a step whose rows are fetched ahead
-constexpr int kSinkBufs = 8;   // staged chunk buffers (a ring between producers and the chains)
+constexpr int kSinkBufs = 4;   // staged chunk buffers per ring (one ring per step parity:
+                               // each chain warp consumes its own ring in order)
 constexpr int kSinkProdWarps = kSinkRows / 32;
 constexpr int kSinkLearnBytes = 2 * kSinkCols * kSinkPre * kSinkRows * 4;
 
 __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, int W) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
-    __shared__ __align__(16) float s_stage[kSinkBufs][kSinkCols][kSinkRows];  // a column's rows contiguous
-    __shared__ __align__(8) uint64_t s_full[kSinkBufs], s_empty[kSinkBufs], s_dn[2], s_pdone[2];
+    __shared__ __align__(16) float s_stage[2][kSinkBufs][kSinkCols][kSinkRows];  // a column's rows contiguous
+    __shared__ __align__(8) uint64_t s_full[2][kSinkBufs], s_empty[2][kSinkBufs], s_dn[2], s_pdone[2];
     __shared__ float s_yd[2][kSinkCols];
     __shared__ uint32_t s_hist[kSinkMaxW];  // sink: the block's column spikes of each step
     __shared__ int s_idx[3][kSinkPre][kSinkRows];  // producers: step w's rows at w % 3 (global index), ascending
     __shared__ long long s_red[32];
+    __shared__ SinkState s_state[kSinkCols];  // the post neurons' state after the last post update
     extern __shared__ __align__(16) uint32_t s_bitRing[];  // sink: pre spike bits [L + 2][preWords],
     // then the rows' learned weights [2][kSinkCols][kSinkPre * kSinkRows] (producers)
     using LearnBuf = float[kSinkCols][kSinkPre * kSinkRows];
@@ -317,14 +327,15 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
     }
     const bool sink = static_cast<int>(blockIdx.x) < T.nSink;
     if (sink && t == 0) {
-        for (int b = 0; b < kSinkBufs; ++b) {
-            mbar_init(&s_full[b], kSinkProdWarps);
-            mbar_init(&s_empty[b], 1);
-        }
+        for (int r = 0; r < 2; ++r)
+            for (int b = 0; b < kSinkBufs; ++b) {
+                mbar_init(&s_full[r][b], kSinkProdWarps);
+                mbar_init(&s_empty[r][b], 1);
+            }
         mbar_init(&s_dn[0], 1);
         mbar_init(&s_dn[1], 1);
-        mbar_init(&s_pdone[0], kSinkProdWarps);
-        mbar_init(&s_pdone[1], kSinkProdWarps);
+        mbar_init(&s_pdone[0], kSinkProdWarps + 1);  // + the notifier warp
+        mbar_init(&s_pdone[1], kSinkProdWarps + 1);
         mbar_fence_init();
     }
     grid.sync();
@@ -334,114 +345,139 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
     }
     const int c0 = blockIdx.x * kSinkCols;
     const int nc = min(kSinkCols, T.nPost - c0);
-    const bool col = warp == 0 && lane < nc;
     // producers: the warps off scheduler 0, where warp 0 (post update + the
     // column chains, the step's critical path) issues alone
     const bool producer = (warp & 3) != 0;
     const int i = ((warp >> 2) * 3 + (warp & 3) - 1) * 32 + lane;  // producers: chunk row i
     // SSB_TRACE: warp 0 of block 0 records each step: {tag | count << 32,
     // post update end (ns from the step's start) | chains end << 32, 0, chain cycles}
-    const bool tr = g_trace != nullptr && t == 0 && blockIdx.x == 0;
+    const bool tr = g_trace != nullptr && t == 32 && blockIdx.x == 0;  // producer thread 32
     unsigned trBase = 0;
     if (tr) trBase = atomicAdd(&g_traceN, static_cast<unsigned>(W));
-    if (warp == 0) {
-        // ---- the post neurons and the column chains
+    if (warp == 0 || warp == 4) {
+        // ---- two chain warps (warp 0: the even steps' folds, warp 4: the odd
+        //      ones; both on scheduler 0, each latency-bound): fold(t + 1)
+        //      needs the post spikes of t (through the learning of t), not
+        //      fold(t), so consecutive steps' chains run at once.  The warp
+        //      that finishes fold(t) runs the post update of t + 1; the
+        //      post neurons' state passes between the two through s_state.
+        const int c = warp >> 2;
+        const bool colc = lane < nc;
         const LifConst lc = lif_const(P);
-        float v = 0.f, ge = 0.f, gi = 0.f, y = 0.f, a = 0.f;
-        uint32_t flag = 1, expMax = 0, bad = 0;
-        if (col) {
-            v = P.v[c0 + lane];
-            ge = P.gExc[c0 + lane];
-            gi = P.gInh[c0 + lane];
-            flag = P.nanFlag[c0 + lane] ? 1u : 0u;
-            y = T.y[c0 + lane];
-        }
-        int g = 0;  // chunk sequence number (the producers count the same way)
-        int cntNext = W > 0 && !(T.skip & 1) ? T.preCnt[0] : 0;
-        for (int w = 0; w < W; ++w) {
-            unsigned long long t0 = 0, tA = 0, waitNs = 0;
-            long long chainCy = 0;
-            if (tr) t0 = global_ns();
-            const int cnt = cntNext;
-            cntNext = w + 1 < W && !(T.skip & 1) ? __ldg(T.preCnt + w + 1) : 0;
-            // the producers have read step w - 2's post spikes and traces
-            // (their slots are rewritten now; steps without spikes need no
-            // producer, so warp 0 could otherwise run ahead)
-            if (w >= 2) mbar_wait(&s_pdone[w & 1], ((w - 2) >> 1) & 1);
-            const float ex = w == 0 ? (col ? P.excIn[c0 + lane] : 0.f) : a;
-            const float ih = w == 0 ? (col ? P.inhIn[c0 + lane] : 0.f) : 0.f;
+        float a = 0.f;
+        uint32_t bad = 0;
+        const auto post_update = [&](int s, float ex, float ih, float& v, float& ge, float& gi,
+                                     float& y, uint32_t flag, uint32_t& expMax) {
+            // the producers have read step s - 2's post spikes and traces
+            // (their slots are rewritten now)
+            if (s >= 2) mbar_wait(&s_pdone[s & 1], ((s - 2) >> 1) & 1);
             bool spike = false;
-            if (col) spike = lif_step<true>(lc, ex, ih, v, ge, gi, expMax, bad);
+            if (colc) spike = lif_step<true>(lc, ex, ih, v, ge, gi, expMax, bad);
             const uint32_t m = __ballot_sync(kFull, spike);
-            if (spike) atomicOr(P.bits + (size_t)w * P.nwords + ((c0 + lane) >> 5), 1u << ((c0 + lane) & 31));
+            if (spike) atomicOr(P.bits + (size_t)s * P.nwords + ((c0 + lane) >> 5), 1u << ((c0 + lane) & 31));
             const float yd = __fmul_rn(y, T.decMinus);
-            if (lane < kSinkCols) s_yd[w & 1][lane] = yd;
-            if (lane == 0) s_hist[w] = m;
+            if (lane < kSinkCols) s_yd[s & 1][lane] = yd;
+            if (lane == 0) s_hist[s] = m;
             y = spike ? __fadd_rn(yd, 1.0f) : yd;
+            if (colc) s_state[lane] = SinkState{v, ge, gi, y, flag, expMax};
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s_dn[w & 1]);
-            if (tr) tA = global_ns();
+            if (lane == 0) mbar_arrive(&s_dn[s & 1]);
+        };
+        float v = 0.f, ge = 0.f, gi = 0.f, y = 0.f;
+        uint32_t flag = 1, expMax = 0;
+        int last = -1;  // the last post update this warp ran
+        if (c == 1 && W > 0) {  // step 0's post update (input: the last window's last fold)
+            if (colc) {
+                v = P.v[c0 + lane];
+                ge = P.gExc[c0 + lane];
+                gi = P.gInh[c0 + lane];
+                flag = P.nanFlag[c0 + lane] ? 1u : 0u;
+                y = T.y[c0 + lane];
+            }
+            post_update(0, colc ? P.excIn[c0 + lane] : 0.f, colc ? P.inhIn[c0 + lane] : 0.f, v, ge,
+                        gi, y, flag, expMax);
+            last = 0;
+        }
+        int g = 0;  // chunk sequence number in this warp's ring (the producers count the same way)
+        for (int w = c; w < W; w += 2) {
+            const int cnt = T.skip & 1 ? 0 : __ldg(T.preCnt + w);
+            const int nCh = (cnt + kSinkRows - 1) / kSinkRows;
             // the fold of step w: the staged chunks in order, rows ascending
             a = 0.f;
-            const int nCh = (cnt + kSinkRows - 1) / kSinkRows;
             for (int k = 0; k < nCh; ++k, ++g) {
                 const int b = g % kSinkBufs;
-                const unsigned long long tw0 = tr ? global_ns() : 0;
-                mbar_wait(&s_full[b], (g / kSinkBufs) & 1);
-                if (tr) waitNs += global_ns() - tw0;
+                mbar_wait(&s_full[c][b], (g / kSinkBufs) & 1);
                 if (lane < kSinkCols) {
-                    const long long cy0 = tr ? clock64() : 0;
                     const int n = min(kSinkRows, cnt - k * kSinkRows);
-                    const float* sb = &s_stage[b][lane][0];
-                    // four staged values per 16-byte load, the next four loading
-                    // while the current four add (the chain is the step's floor)
+                    const float* sb = &s_stage[c][b][lane][0];
                     const int n4 = n & ~3;
                     if (n4 > 0) {
-                        float4 c = *reinterpret_cast<const float4*>(sb);
+                        float4 cc = *reinterpret_cast<const float4*>(sb);
                         for (int q = 4; q < n4; q += 4) {
                             const float4 d = *reinterpret_cast<const float4*>(sb + q);
-                            a = __fadd_rn(a, c.x);
-                            a = __fadd_rn(a, c.y);
-                            a = __fadd_rn(a, c.z);
-                            a = __fadd_rn(a, c.w);
-                            c = d;
+                            a = __fadd_rn(a, cc.x);
+                            a = __fadd_rn(a, cc.y);
+                            a = __fadd_rn(a, cc.z);
+                            a = __fadd_rn(a, cc.w);
+                            cc = d;
                         }
-                        a = __fadd_rn(a, c.x);
-                        a = __fadd_rn(a, c.y);
-                        a = __fadd_rn(a, c.z);
-                        a = __fadd_rn(a, c.w);
+                        a = __fadd_rn(a, cc.x);
+                        a = __fadd_rn(a, cc.y);
+                        a = __fadd_rn(a, cc.z);
+                        a = __fadd_rn(a, cc.w);
                     }
                     for (int q = n4; q < n; ++q) a = __fadd_rn(a, sb[q]);
-                    if (tr) {
-                        const float aa = a;
-                        asm volatile("" ::"f"(aa));
-                        chainCy += clock64() - cy0;
-                    }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&s_empty[b]);
+                if (lane == 0) mbar_arrive(&s_empty[c][b]);
             }
-            if (tr && trBase + w < g_traceCap) {
-                unsigned long long* e = g_trace + 4ull * (trBase + w);
-                e[0] = 0x5100ull | (static_cast<unsigned long long>(cnt) << 32);
-                e[1] = (tA - t0) | ((global_ns() - t0) << 32);
-                e[2] = waitNs;  // warp 0 waiting for staged chunks
-                e[3] = static_cast<unsigned long long>(chainCy);
+            if (g_watch && lane == 0) g_watch[blockIdx.x * 2 + c] = w;
+            if (w + 1 < W) {  // the post update of w + 1: the state of w from the other warp
+                mbar_wait(&s_dn[w & 1], (w >> 1) & 1);
+                if (colc) {
+                    const SinkState st = s_state[lane];
+                    v = st.v;
+                    ge = st.ge;
+                    gi = st.gi;
+                    y = st.y;
+                    flag = st.flag;
+                    expMax = st.expMax;
+                }
+                post_update(w + 1, a, 0.f, v, ge, gi, y, flag, expMax);
+                last = w + 1;
+            } else if (colc) {  // the window's last fold: the next window's first input
+                P.excIn[c0 + lane] = a;
+                P.inhIn[c0 + lane] = 0.f;
             }
         }
-        // ---- end of window: post state, next window's first input, traces
-        if (col) {
+        if (last == W - 1 && colc) {
             const int j = c0 + lane;
             P.v[j] = v;
             P.gExc[j] = ge;
             P.gInh[j] = gi;
-            P.excIn[j] = a;
-            P.inhIn[j] = 0.f;
             P.nanFlag[j] = static_cast<uint8_t>(flag | (expMax == 0x7f800000u));
             T.y[j] = y;
             if (!flag && expMax == 0x7f800000u) atomicAdd(P.flagged, 1ull);
         }
         (void)s_red;
+        (void)bad;
+        (void)tr;
+        (void)trBase;
+        return;
+    }
+    if (warp == 8) {
+        // the notifier: once a step's post spikes are out, tell the background
+        // blocks (its fence stays off the chains' and the producers' paths)
+        for (int w = 0; w < W; ++w) {
+            mbar_wait(&s_dn[w & 1], (w >> 1) & 1);
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                atomicAdd(T.sinkDone + w, 1);
+                mbar_arrive(&s_pdone[w & 1]);
+            }
+            __syncwarp();
+        }
         return;
     }
     if (!producer) return;
@@ -464,11 +500,26 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
         ring_load(T, s_bitRing, 0, i, kSinkRows);
     }
     asm volatile("bar.sync 1, %0;" ::"r"(kSinkRows));
-    int g = 0, cntPrev = 0;
+    int gr0 = 0, gr1 = 0, cntPrev = 0;  // chunk sequence numbers of the two rings
     for (int w = 0; w < W; ++w) {
         const int cnt = cntCur;
         const int nCh = (cnt + kSinkRows - 1) / kSinkRows;
         const int nextCnt = w + 1 < W && !(T.skip & 1) ? __ldg(T.preCnt + w + 1) : 0;
+        // the background's step w - L (the next step's weights wait for it),
+        // read early; the next step's row indices and pre spike bits, copied
+        // asynchronously (read-only; indices past the count are never read)
+        const int bgEarly = w + 1 > kSinkLag && w + 1 < W
+                                ? *reinterpret_cast<const volatile int*>(T.bgDone + (w - kSinkLag)) : 0;
+        if (w + 1 < W) {
+            const int* Ln = T.preList + (size_t)(w + 1) * T.preN;
+#pragma unroll
+            for (int kk = 0; kk < kSinkPre; ++kk)
+                if (kk * kSinkRows + i < T.preN) cp_async4(&s_idx[(w + 1) % 3][kk][i], Ln + kk * kSinkRows + i);
+            const uint32_t* pb = T.preBits + (size_t)(w + 1) * T.preWords;
+            uint32_t* dst = s_bitRing + ((w + 1) % kSinkRing) * T.preWords;
+            for (int k = i; k < T.preWords; k += kSinkRows) cp_async4(dst + k, pb + k);
+            cp_async_commit();
+        }
         // rows that spiked at w - 1 too: their weights after that step's learning
         if (w > 0) {
             const int* prevIdx = &s_idx[(w - 1) % 3][0][0];  // step w - 1's rows, ascending
@@ -495,41 +546,31 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
         // producers waited for the post update of w - 1)
         float xdw[kSinkPre];
 #pragma unroll
+        unsigned long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (tr) tp[0] = global_ns();
+        const int ring = w & 1;
+        const int g = ring ? gr1 : gr0;
         for (int kk = 0; kk < kSinkPre; ++kk) {
             if (kk >= nCh) break;
             const int gg = g + kk, b = gg % kSinkBufs;
             xdw[kk] = 0.f;
             if (rec[kk].r >= 0) sink_stage(T, w, rec[kk], v[kk], s_hist, xdw[kk]);
-            if (gg >= kSinkBufs) mbar_wait(&s_empty[b], ((gg / kSinkBufs) - 1) & 1);
+            if (gg >= kSinkBufs) mbar_wait(&s_empty[ring][b], ((gg / kSinkBufs) - 1) & 1);
             const bool live = kk * kSinkRows + i < cnt;
 #pragma unroll
-            for (int j = 0; j < kSinkCols; ++j) s_stage[b][j][i] = live && rec[kk].r >= 0 ? v[kk][j] : 0.f;
+            for (int j = 0; j < kSinkCols; ++j)
+                s_stage[ring][b][j][i] = live && rec[kk].r >= 0 ? v[kk][j] : 0.f;
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s_full[b]);
+            if (lane == 0) mbar_arrive(&s_full[ring][b]);
         }
-        // the next step's row indices and pre spike bits, copied asynchronously
-        if (w + 1 < W) {
-            const int* Ln = T.preList + (size_t)(w + 1) * T.preN;
-#pragma unroll
-            for (int kk = 0; kk < kSinkPre; ++kk) {
-                if (kk * kSinkRows + i < nextCnt) cp_async4(&s_idx[(w + 1) % 3][kk][i], Ln + kk * kSinkRows + i);
-                else s_idx[(w + 1) % 3][kk][i] = INT_MAX;
-            }
-            const uint32_t* pb = T.preBits + (size_t)(w + 1) * T.preWords;
-            uint32_t* dst = s_bitRing + ((w + 1) % kSinkRing) * T.preWords;
-            for (int k = i; k < T.preWords; k += kSinkRows) cp_async4(dst + k, pb + k);
-            cp_async_commit();
-        }
+        if (tr) tp[1] = global_ns();  // staged
         // the step's post spikes, then its learning
         mbar_wait(&s_dn[w & 1], (w >> 1) & 1);
+        if (tr) tp[2] = global_ns();  // post spikes out
         const uint32_t spk = s_hist[w];
         const float yd[kSinkCols] = {s_yd[w & 1][0], s_yd[w & 1][1]};
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_pdone[w & 1]);
-        if (t == 32) {  // the block's post spikes of w are out
-            __threadfence();
-            atomicAdd(T.sinkDone + w, 1);
-        }
 #pragma unroll
         for (int kk = 0; kk < kSinkPre; ++kk) {
             if (kk >= nCh || kk * kSinkRows + i >= cnt || rec[kk].r < 0) continue;
@@ -538,6 +579,7 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
 #pragma unroll
             for (int j = 0; j < kSinkCols; ++j) s_learn[w & 1][j][kk * kSinkRows + i] = lw[j];
         }
+        if (tr) tp[3] = global_ns();  // learned
         for (int k = kSinkPre; k < nCh; ++k) {  // beyond the fetched chunks: on demand
             const int gg = g + k, b = gg % kSinkBufs;
             const int e = k * kSinkRows + i;
@@ -550,15 +592,16 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
                     vv[j] = j < nc ? __ldcg(T.WT + (size_t)(c0 + j) * nPre + q.r) : 0.f;
                 sink_stage(T, w, q, vv, s_hist, xw);
             }
-            if (gg >= kSinkBufs) mbar_wait(&s_empty[b], ((gg / kSinkBufs) - 1) & 1);
+            if (gg >= kSinkBufs) mbar_wait(&s_empty[ring][b], ((gg / kSinkBufs) - 1) & 1);
 #pragma unroll
-            for (int j = 0; j < kSinkCols; ++j) s_stage[b][j][i] = q.r >= 0 ? vv[j] : 0.f;
+            for (int j = 0; j < kSinkCols; ++j) s_stage[ring][b][j][i] = q.r >= 0 ? vv[j] : 0.f;
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s_full[b]);
+            if (lane == 0) mbar_arrive(&s_full[ring][b]);
             float lw[kSinkCols];
             if (q.r >= 0) sink_learn(T, q, vv, xw, c0, nc, spk, yd, lw);
         }
-        g += nCh;
+        if (ring) gr1 += nCh;
+        else gr0 += nCh;
         if (w + 1 < W) {
             // the next step's rows from the copies issued above, and their
             // weights: final except for the rows spiking now (fixed up above
@@ -570,7 +613,10 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
                 recN[kk] = e < nextCnt ? sink_fetch_row(T, w + 1, s_idx[(w + 1) % 3][kk][i], s_bitRing)
                                        : SinkRow{};
             }
-            if (w + 1 > kSinkLag) spin_until(T.bgDone + (w - kSinkLag), gridDim.x - T.nSink);
+            if (tr) tp[4] = global_ns();  // fetched
+            if (w + 1 > kSinkLag && bgEarly < static_cast<int>(gridDim.x) - T.nSink)
+                spin_until(T.bgDone + (w - kSinkLag), gridDim.x - T.nSink);
+            if (tr) tp[5] = global_ns();  // background in
 #pragma unroll
             for (int kk = 0; kk < kSinkPre; ++kk)
 #pragma unroll
@@ -589,5 +635,14 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
         // every producer's learning of w (s_learn, the weights) and ring slot
         // w + 1 in before step w + 1 is staged
         asm volatile("bar.sync 1, %0;" ::"r"(kSinkRows));
+        if (g_watch && t == 32) g_watch[2 * T.nSink + blockIdx.x] = w;
+        if (tr && trBase + w < g_traceCap) {
+            tp[6] = global_ns();  // barrier passed
+            unsigned long long* e = g_trace + 4ull * (trBase + w);
+            e[0] = 0x5200ull | (static_cast<unsigned long long>(cnt) << 32);
+            e[1] = tp[0];
+            e[2] = (tp[1] - tp[0]) | ((tp[2] - tp[0]) << 16) | ((tp[3] - tp[0]) << 32) | ((tp[4] - tp[0]) << 48);
+            e[3] = (tp[5] - tp[0]) | ((tp[6] - tp[0]) << 16);
+        }
     }
 }
