@@ -156,7 +156,38 @@ __global__ void __launch_bounds__(kCycThreads, 1) cyclic_block_kernel(const CycD
             }
             if (nRows == 0) continue;
             __syncthreads();
-            // post-centric: each post folds the rows in order (coalesced rows)
+            // post-centric: each post folds the rows in order (coalesced rows);
+            // four posts per thread with 16-byte row loads where the rows allow
+            if ((G.nPost & 3) == 0) {
+                const int nq = G.nPost >> 2;
+                for (int jq = t; jq < nq; jq += blockDim.x) {
+                    const int j = jq << 2;
+                    float a0 = s_acc[G.accBase + j], a1 = s_acc[G.accBase + j + 1];
+                    float a2 = s_acc[G.accBase + j + 2], a3 = s_acc[G.accBase + j + 3];
+                    for (int q0 = 0; q0 < nRows; q0 += 4) {
+                        float4 x[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            x[u] = q0 + u < nRows
+                                       ? __ldg(reinterpret_cast<const float4*>(G.W + (size_t)s_rows[q0 + u] * G.nPost + j))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (q0 + u < nRows) {
+                                a0 = __fadd_rn(a0, x[u].x);
+                                a1 = __fadd_rn(a1, x[u].y);
+                                a2 = __fadd_rn(a2, x[u].z);
+                                a3 = __fadd_rn(a3, x[u].w);
+                            }
+                    }
+                    s_acc[G.accBase + j] = a0;
+                    s_acc[G.accBase + j + 1] = a1;
+                    s_acc[G.accBase + j + 2] = a2;
+                    s_acc[G.accBase + j + 3] = a3;
+                }
+                __syncthreads();
+                continue;
+            }
             for (int j = t; j < G.nPost; j += blockDim.x) {
                 float acc = s_acc[G.accBase + j];
                 for (int q0 = 0; q0 < nRows; q0 += 8) {
