@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(kCycThreads, 1) cyclic_block_kernel(const CycD
                                                                       int W) {
     __shared__ CycDev D;
     __shared__ int s_scan[33];
+    __shared__ int s_gStart[kCycMaxGroups + 1];  // a wave's groups: first row of each in s_rows
     extern __shared__ __align__(16) int s_cyc[];
     float* s_acc = reinterpret_cast<float*>(s_cyc);                      // [kCycMaxAcc]
     int* s_rows = s_cyc + kCycMaxAcc;                                    // [kCycMaxRows]
@@ -139,69 +140,104 @@ __global__ void __launch_bounds__(kCycThreads, 1) cyclic_block_kernel(const CycD
         // ---- zero the accumulators, then every group's contributions in spec
         //      order (engine.cpp:341-355), each folded into its accumulators
         for (int i = t; i < nAcc; i += blockDim.x) s_acc[i] = 0.f;
-        for (int gq = 0; gq < D.nGroups; ++gq) {
-            const CycGroup& G = D.groups[gq];
-            if (G.accBase < 0) continue;  // into a Poisson population: no input to keep
-            // the group's spiking pre rows, ascending (a barrier ends the scans)
-            const int base = D.pops[G.pre].base + G.preOffset;
+        // groups in waves: consecutive groups (spec order) into distinct
+        // accumulators fold at once (a group into the same accumulator as an
+        // earlier one waits for the next wave); one ordered compaction of all
+        // the wave's candidate rows
+        for (int g0 = 0; g0 < D.nGroups;) {
+            int g1 = g0, cand = 0;
+            while (g1 < D.nGroups) {
+                const CycGroup& G = D.groups[g1];
+                bool clash = cand + G.preCount > kCycMaxRows && g1 > g0;
+                for (int h = g0; h < g1 && !clash; ++h)
+                    clash = D.groups[h].accBase >= 0 && D.groups[h].accBase == G.accBase;
+                if (clash) break;
+                cand += G.preCount;
+                ++g1;
+            }
+            // the wave's spiking rows: group by group, rows ascending
             int nRows = 0;
-            for (int r0 = 0; r0 < G.preCount; r0 += blockDim.x) {
-                const int r = r0 + t;
-                const int x = base + r;
-                const bool on = r < G.preCount && ((s_bits[x >> 5] >> (x & 31)) & 1u);
+            for (int c0 = 0; c0 < cand; c0 += blockDim.x) {
+                const int cidx = c0 + t;
+                bool on = false;
+                int r = 0, gl = 0;
+                if (cidx < cand) {
+                    int off = cidx;
+                    gl = g0;
+                    while (off >= D.groups[gl].preCount) off -= D.groups[gl++].preCount;
+                    r = off;
+                    const CycGroup& G = D.groups[gl];
+                    const int x = D.pops[G.pre].base + G.preOffset + r;
+                    on = G.accBase >= 0 && ((s_bits[x >> 5] >> (x & 31)) & 1u);
+                }
                 int total;
                 const int pos = block_exclusive_scan(on ? 1 : 0, total, s_scan);
-                if (on) s_rows[nRows + pos] = r;
+                if (on) s_rows[nRows + pos] = r | ((gl - g0) << 24);
+                if (cidx < cand && r == 0) s_gStart[gl - g0] = nRows + pos;  // first row of the group
                 nRows += total;
             }
-            if (nRows == 0) continue;
+            if (t == 0) s_gStart[g1 - g0] = nRows;
             __syncthreads();
-            // post-centric: each post folds the rows in order (coalesced rows);
-            // four posts per thread with 16-byte row loads where the rows allow
-            if ((G.nPost & 3) == 0) {
-                const int nq = G.nPost >> 2;
-                for (int jq = t; jq < nq; jq += blockDim.x) {
-                    const int j = jq << 2;
-                    float a0 = s_acc[G.accBase + j], a1 = s_acc[G.accBase + j + 1];
-                    float a2 = s_acc[G.accBase + j + 2], a3 = s_acc[G.accBase + j + 3];
-                    for (int q0 = 0; q0 < nRows; q0 += 4) {
-                        float4 x[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            x[u] = q0 + u < nRows
-                                       ? __ldg(reinterpret_cast<const float4*>(G.W + (size_t)s_rows[q0 + u] * G.nPost + j))
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (q0 + u < nRows) {
-                                a0 = __fadd_rn(a0, x[u].x);
-                                a1 = __fadd_rn(a1, x[u].y);
-                                a2 = __fadd_rn(a2, x[u].z);
-                                a3 = __fadd_rn(a3, x[u].w);
-                            }
+            if (nRows > 0) {
+                // post-centric folds: each post folds its group's rows in order;
+                // four posts per item (16-byte row loads) where the rows allow
+                int items = 0;
+                for (int h = g0; h < g1; ++h)
+                    items += D.groups[h].accBase < 0 ? 0 : ((D.groups[h].nPost & 3) == 0 ? D.groups[h].nPost >> 2
+                                                                                        : D.groups[h].nPost);
+                for (int it = t; it < items; it += blockDim.x) {
+                    int h = g0, off = it;
+                    for (;;) {
+                        const CycGroup& G = D.groups[h];
+                        const int ni = G.accBase < 0 ? 0 : ((G.nPost & 3) == 0 ? G.nPost >> 2 : G.nPost);
+                        if (off < ni) break;
+                        off -= ni;
+                        ++h;
                     }
-                    s_acc[G.accBase + j] = a0;
-                    s_acc[G.accBase + j + 1] = a1;
-                    s_acc[G.accBase + j + 2] = a2;
-                    s_acc[G.accBase + j + 3] = a3;
-                }
-                __syncthreads();
-                continue;
-            }
-            for (int j = t; j < G.nPost; j += blockDim.x) {
-                float acc = s_acc[G.accBase + j];
-                for (int q0 = 0; q0 < nRows; q0 += 8) {
-                    float x[8];
+                    const CycGroup& G = D.groups[h];
+                    const int q0 = s_gStart[h - g0], q1 = s_gStart[h - g0 + 1];
+                    if ((G.nPost & 3) == 0) {
+                        const int j = off << 2;
+                        float a0 = s_acc[G.accBase + j], a1 = s_acc[G.accBase + j + 1];
+                        float a2 = s_acc[G.accBase + j + 2], a3 = s_acc[G.accBase + j + 3];
+                        for (int q = q0; q < q1; q += 4) {
+                            float4 x[4];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        x[u] = q0 + u < nRows ? __ldg(G.W + (size_t)s_rows[q0 + u] * G.nPost + j) : 0.f;
+                            for (int u = 0; u < 4; ++u)
+                                x[u] = q + u < q1 ? __ldg(reinterpret_cast<const float4*>(
+                                                        G.W + (size_t)(s_rows[q + u] & 0xffffff) * G.nPost + j))
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        if (q0 + u < nRows) acc = __fadd_rn(acc, x[u]);
+                            for (int u = 0; u < 4; ++u)
+                                if (q + u < q1) {
+                                    a0 = __fadd_rn(a0, x[u].x);
+                                    a1 = __fadd_rn(a1, x[u].y);
+                                    a2 = __fadd_rn(a2, x[u].z);
+                                    a3 = __fadd_rn(a3, x[u].w);
+                                }
+                        }
+                        s_acc[G.accBase + j] = a0;
+                        s_acc[G.accBase + j + 1] = a1;
+                        s_acc[G.accBase + j + 2] = a2;
+                        s_acc[G.accBase + j + 3] = a3;
+                    } else {
+                        const int j = off;
+                        float acc = s_acc[G.accBase + j];
+                        for (int q = q0; q < q1; q += 8) {
+                            float x[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                x[u] = q + u < q1 ? __ldg(G.W + (size_t)(s_rows[q + u] & 0xffffff) * G.nPost + j) : 0.f;
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                if (q + u < q1) acc = __fadd_rn(acc, x[u]);
+                        }
+                        s_acc[G.accBase + j] = acc;
+                    }
                 }
-                s_acc[G.accBase + j] = acc;
             }
             __syncthreads();
+            g0 = g1;
         }
     }
     // ---- end of window: state, the next window's first inputs, NaN flags
