@@ -10,7 +10,7 @@
 // block barriers (reference engine.cpp:316-356 per step):
 //   advance + NaN flag + threshold of every population (a neuron per thread
 //     slot, state in registers; Izhikevich noise and Poisson spikes are drawn
-//     for the window beforehand by gaussian_window_kernel /
+//     for the window beforehand by gaussian_draw/transform_kernel and
 //     poisson_window_kernel, in the reference's stream order);
 //   the step's spike bits (shared memory and the window's bitmask rows);
 //   the inputs of step t + 1, group by group in spec order: every post folds

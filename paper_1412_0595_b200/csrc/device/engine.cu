@@ -219,7 +219,7 @@ bool kernel_attributes(const std::string& name, int& regs, int& sharedBytes, int
         e = cudaFuncGetAttributes(&a, ssbk::condlif_pair_window_kernel);
     else if (name == "izh_window") e = cudaFuncGetAttributes(&a, ssbk::izh_window_kernel);
     else if (name == "hh_window") e = cudaFuncGetAttributes(&a, ssbk::hh_window_kernel);
-    else if (name == "gaussian_window") e = cudaFuncGetAttributes(&a, ssbk::gaussian_window_kernel);
+    else if (name == "gaussian_window") e = cudaFuncGetAttributes(&a, ssbk::gaussian_draw_kernel);
     else if (name == "poisson_window") e = cudaFuncGetAttributes(&a, ssbk::poisson_window_kernel);
     else if (name == "dense_window") e = cudaFuncGetAttributes(&a, ssbk::dense_window_kernel);
     else if (name == "dense_window_warp")
@@ -538,6 +538,11 @@ struct DeviceEngine::Impl {
     void post_launch(int W, int M, std::int64_t add);
     void enqueue_tail(int W, int b, cudaStream_t s);
     void enqueue_cyclic(int W, int M);
+    // the Gaussian transform kernel's blocks for a window of W steps of n neurons
+    int gauss_grid(int n, int W) const {
+        const long long pairs = (static_cast<long long>(W) * n + 1) / 2;
+        return static_cast<int>(std::max<long long>(1, std::min<long long>((pairs + 255) / 256, 4ll * smCount)));
+    }
     void enqueue_windows(int W, int M);
     void run_windows(int W, int M);
     void flush_raster(bool wait = false);
@@ -1166,7 +1171,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             d.spare = alloc<double>(1);
             d.hasSpare = alloc<int>(1);
             d.noiseIn = alloc<float>(static_cast<std::size_t>(Wmax) * n);
-            d.draws = alloc<unsigned long long>(static_cast<std::size_t>(Wmax) * n + 2);
+            // the window's uniforms, then the draw kernel's stash (3 words)
+            d.draws = alloc<unsigned long long>(static_cast<std::size_t>(Wmax) * n + 5);
             CK(cudaStreamSynchronize(stream));
         }
         for (int a = 0; a < 2; ++a)
@@ -1735,8 +1741,11 @@ void DeviceEngine::Impl::enqueue_pop(int pi, int W, int b, cudaStream_t sg, cuda
             });
         };
         if (P.kind == kIzhikevich) {
-            launch("gaussian_window:" + P.name, [&] {
-                ssbk::gaussian_window_kernel<<<1, 320, 0, sm>>>(K, W);
+            launch("gaussian_draw:" + P.name, [&] {
+                ssbk::gaussian_draw_kernel<<<1, 320, 0, sm>>>(K, W);
+            });
+            launch("gaussian_transform:" + P.name, [&] {
+                ssbk::gaussian_transform_kernel<<<gauss_grid(P.n, W), 256, 0, sm>>>(K, W);
             });
             update("izh_window:", ssbk::izh_window_kernel);
         } else if (P.kind == kTraubMiles) {
@@ -1995,8 +2004,11 @@ void DeviceEngine::Impl::enqueue_cyclic(int W, int M) {
                         K, W, ssbk::kAccNone, ssbk::kAccNone, inSmem);
                 });
             } else if (P.kind == kIzhikevich && P.n > 0) {
-                launch("gaussian_window:" + P.name, [&] {
-                    ssbk::gaussian_window_kernel<<<1, 320, 0, gs>>>(K, W);
+                launch("gaussian_draw:" + P.name, [&] {
+                    ssbk::gaussian_draw_kernel<<<1, 320, 0, gs>>>(K, W);
+                });
+                launch("gaussian_transform:" + P.name, [&] {
+                    ssbk::gaussian_transform_kernel<<<gauss_grid(P.n, W), 256, 0, gs>>>(K, W);
                 });
             }
         }
