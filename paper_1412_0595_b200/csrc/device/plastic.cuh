@@ -17,12 +17,20 @@
 // weights as they are before step t's learning.  The weights are kept
 // transposed [nPost][nPre] (a column contiguous).  One cooperative kernel per
 // window, two roles, no grid-wide barrier:
-//   sink blocks (kSinkCols post columns each): per step t, the post update
-//     (input: the block's own fold of t - 1; the mushroom body's DN fire in
-//     volleys), then for every row spiking at t the potentiations it still
-//     owes from steps t - L .. t - 1 (it was silent since, a column spiked),
-//     the staged value for the fold, and its learning at t; warp 0's lanes run
-//     the column chains over the staged chunks, rows ascending;
+//   sink blocks (kSinkCols post columns each), warps in four parts:
+//     two chain warps (warp 0: even steps, warp 4: odd steps) fold the staged
+//     chunks of their steps, rows ascending, and the warp that finishes
+//     fold(t) runs the post update of t + 1 (fold(t + 1) needs the post spikes
+//     of t, not fold(t), so consecutive steps' chains overlap; the post state
+//     passes between them in shared memory);
+//     twelve producer warps stage every row spiking at t -- its weights after
+//     the potentiations it still owes from steps t - L .. t - 1 (silent since,
+//     a column spiked) -- into a per-parity ring of chunk buffers
+//     (full/empty mbarriers), then, once t's post spikes are out, store the
+//     row's learning at t; a step's rows and weights load during the step
+//     before (rows that spiked then take their learned values from shared
+//     memory);
+//     a notifier warp tells the background blocks when t's post spikes are out;
 //   background blocks: the potentiation of step s for the rows silent through
 //     s .. s + L (a volley step rewrites the whole matrix), up to L steps behind
 //     the sink blocks -- so a volley's matrix pass overlaps the next steps.
@@ -37,8 +45,8 @@
 // (sink_trace_kernel, [W][nPre]).
 constexpr int kSinkThreads = 512;
 constexpr int kSinkCols = 2;                      // post columns per sink block
-// producers: the warps off scheduler 0, where warp 0's column chains (the
-// step's critical path) issue alone; a staged chunk is a row per producer
+// producers: the warps off scheduler 0, where the chain warps (the step's
+// critical path) issue; a staged chunk is a row per producer
 constexpr int kSinkRows = kSinkThreads / 4 * 3;   // 384
 constexpr int kSinkLag = 4;                       // L: the background's lag in steps
 constexpr int kTailMaxPost = 128;
