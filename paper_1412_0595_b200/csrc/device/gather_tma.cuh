@@ -359,21 +359,18 @@ __global__ void __launch_bounds__(256) propagate_crs_sliced_kernel(
         float a = j < nPost ? acc[j] : 0.f;
         int k = 0;
         constexpr int U = 16;  // loads in flight per lane (DRAM latency x bandwidth)
-        for (; k + U <= len; k += U) {
+        for (; k < len; k += U) {  // the last round predicated (no load-by-load tail)
             int r[U];
             float v[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                r[u] = __ldg(R + (k + u) * 32);
-                v[u] = __ldg(V + (k + u) * 32);
+                const bool in = k + u < len;
+                r[u] = in ? __ldg(R + (k + u) * 32) : -1;
+                v[u] = in ? __ldg(V + (k + u) * 32) : 0.f;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u)
                 if (r[u] >= 0 && ((s_spk[r[u] >> 5] >> (r[u] & 31)) & 1u)) a = __fadd_rn(a, v[u]);
-        }
-        for (; k < len; ++k) {
-            const int r = __ldg(R + k * 32);
-            if (r >= 0 && ((s_spk[r >> 5] >> (r & 31)) & 1u)) a = __fadd_rn(a, __ldg(V + k * 32));
         }
         if (j < nPost) acc[j] = a;
     }
