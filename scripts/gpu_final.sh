@@ -1,6 +1,7 @@
-# round-end evidence: GPU suite, full bench line (default flags), launch list
+# round-end evidence: GPU suite, smoke, full bench line (default flags)
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1
 tail -3 gpurun_out/gputest.log
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
 tail -c 600 gpurun_out/bench_final.json
