@@ -16,6 +16,7 @@
 #include <utility>
 #include <numeric>
 #include <string>
+#include <atomic>
 #include <thread>
 #include <vector>
 
@@ -357,6 +358,10 @@ struct DeviceEngine::Impl {
         int tailSmem = 0;
     };
     std::vector<StdpRt> stdp;
+    // SSB_SINK_WATCH (diagnostic): a host thread printing the plastic sink's progress
+    std::thread watchThread;
+    std::atomic<bool> watchStop{false};
+    int* watchHost = nullptr;
     std::vector<ssbk::GroupDev> groupDev;
     std::vector<int> order;
     std::vector<void*> allocations;
@@ -1419,16 +1424,16 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             T.decMinus = g.decMinus;
             T.wMax = g.wMax;
             if (const char* e = std::getenv("SSB_TAIL_SKIP")) T.skip = std::atoi(e);
-            if (std::getenv("SSB_SINK_WATCH")) {  // diagnostic: a thread prints each role's progress
-                int* hw = nullptr;
-                CK(cudaHostAlloc(&hw, 4 * (3 * T.nSink + 1) * sizeof(int), cudaHostAllocMapped));
+            if (std::getenv("SSB_SINK_WATCH") && !watchHost) {  // diagnostic: each role's progress
+                CK(cudaHostAlloc(&watchHost, 4 * (3 * T.nSink + 1) * sizeof(int), cudaHostAllocMapped));
                 int* dw = nullptr;
-                CK(cudaHostGetDevicePointer(&dw, hw, 0));
+                CK(cudaHostGetDevicePointer(&dw, watchHost, 0));
                 CK(cudaMemcpyToSymbol(ssbk::g_watch, &dw, sizeof(dw)));
                 const int ns = T.nSink;
-                std::thread([hw, ns] {
-                    for (;;) {
-                        std::this_thread::sleep_for(std::chrono::seconds(2));
+                int* hw = watchHost;
+                watchThread = std::thread([this, hw, ns] {
+                    while (!watchStop.load()) {
+                        std::this_thread::sleep_for(std::chrono::milliseconds(2000));
                         volatile int* v = hw;
                         std::fprintf(stderr, "watch: bg %d | chains", v[3 * ns]);
                         for (int b = 0; b < std::min(ns, 4); ++b) std::fprintf(stderr, " %d/%d", v[2 * b], v[2 * b + 1]);
@@ -1436,7 +1441,7 @@ void DeviceEngine::Impl::build(const HostNet& net) {
                         for (int b = 0; b < std::min(ns, 4); ++b) std::fprintf(stderr, " %d", v[2 * ns + b]);
                         std::fprintf(stderr, "\n");
                     }
-                }).detach();
+                });
             }
             for (int b = 0; b < nSets; ++b) {
                 L.tdev[b] = T;
@@ -2364,6 +2369,16 @@ void DeviceEngine::lockstep(int W) {
 
 void DeviceEngine::Impl::release() {
     join_copier();
+    if (watchThread.joinable()) {
+        watchStop = true;
+        watchThread.join();
+    }
+    if (watchHost) {
+        int* nul = nullptr;
+        cudaMemcpyToSymbol(ssbk::g_watch, &nul, sizeof(nul));
+        cudaFreeHost(watchHost);
+        watchHost = nullptr;
+    }
     if (traceBuf && !tracePath.empty()) {
         cudaDeviceSynchronize();
         unsigned n = 0;
