@@ -915,7 +915,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
         bool ok = net.pops[p].kind == kCondLif && g.pre != p && g.nPost <= ssbk::kTailMaxPost &&
                   net.pops[p].nGlobal == 0 && net.pops[g.pre].nGlobal == 0 && !g.rowSplit &&
                   cfg.window <= ssbk::kSinkMaxW && xdBytes <= freeB / 4 &&
-                  ssbk::kSinkRing * ((net.pops[g.pre].n + 31) / 32) * 4 + ssbk::kSinkLearnBytes <= 180 * 1024 &&
+                  ssbk::kSinkRing * ((net.pops[g.pre].n + 31) / 32) * 4 + ssbk::kSinkLearnBytes +
+                          ssbk::kSinkIdxBytes <= 180 * 1024 &&
                   tailOf[p] < 0;
         for (const auto& h : net.groups) {
             if (h.pre == p) ok = false;                // a sink
@@ -1391,7 +1392,8 @@ void DeviceEngine::Impl::build(const HostNet& net) {
             ssbk::TailDev T{};
             T.nSink = (g.nPost + ssbk::kSinkCols - 1) / ssbk::kSinkCols;
             // dynamic shared memory: the ring of L + 2 steps' pre spike bits
-            L.tailSmem = (ssbk::kSinkRing * pops[g.pre].nwords + 3) / 4 * 16 + ssbk::kSinkLearnBytes;
+            L.tailSmem = (ssbk::kSinkRing * pops[g.pre].nwords + 3) / 4 * 16 + ssbk::kSinkLearnBytes +
+                         ssbk::kSinkIdxBytes;
             allow_smem(reinterpret_cast<const void*>(&ssbk::sink_step_kernel), L.tailSmem);
             int perSm = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, ssbk::sink_step_kernel,

@@ -43,7 +43,7 @@
 // background applies the last steps' potentiations to every silent row.  The
 // pre traces' decayed values xd[t][r] come from a table the prepass writes
 // (sink_trace_kernel, [W][nPre]).
-constexpr int kSinkThreads = 512;
+constexpr int kSinkThreads = 640;
 constexpr int kSinkCols = 2;                      // post columns per sink block
 // producers: the warps off scheduler 0, where the chain warps (the step's
 // critical path) issue; a staged chunk is a row per producer
@@ -310,6 +310,7 @@ constexpr int kSinkBufs = 4;   // staged chunk buffers per ring (one ring per st
                                // each chain warp consumes its own ring in order)
 constexpr int kSinkProdWarps = kSinkRows / 32;
 constexpr int kSinkLearnBytes = 2 * kSinkCols * kSinkPre * kSinkRows * 4;
+constexpr int kSinkIdxBytes = 3 * kSinkPre * kSinkRows * 4;  // + the rows of three steps
 
 __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, int W) {
     namespace cg = cooperative_groups;
@@ -318,13 +319,15 @@ __global__ void __launch_bounds__(kSinkThreads, 1) sink_step_kernel(TailDev T, i
     __shared__ __align__(8) uint64_t s_full[2][kSinkBufs], s_empty[2][kSinkBufs], s_dn[2], s_pdone[2];
     __shared__ float s_yd[2][kSinkCols];
     __shared__ uint32_t s_hist[kSinkMaxW];  // sink: the block's column spikes of each step
-    __shared__ int s_idx[3][kSinkPre][kSinkRows];  // producers: step w's rows at w % 3 (global index), ascending
     __shared__ long long s_red[32];
     __shared__ SinkState s_state[kSinkCols];  // the post neurons' state after the last post update
     extern __shared__ __align__(16) uint32_t s_bitRing[];  // sink: pre spike bits [L + 2][preWords],
     // then the rows' learned weights [2][kSinkCols][kSinkPre * kSinkRows] (producers)
     using LearnBuf = float[kSinkCols][kSinkPre * kSinkRows];
     LearnBuf* s_learn = reinterpret_cast<LearnBuf*>(s_bitRing + ((kSinkRing * T.preWords + 3) & ~3));
+    // producers: step w's rows at w % 3 (global index), ascending
+    using IdxBuf = int[kSinkPre][kSinkRows];
+    IdxBuf* s_idx = reinterpret_cast<IdxBuf*>(reinterpret_cast<char*>(s_learn) + kSinkLearnBytes);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const PopDev& P = T.P;
     const int nPre = T.nPre;
