@@ -23,7 +23,7 @@
 //     fold(t) runs the post update of t + 1 (fold(t + 1) needs the post spikes
 //     of t, not fold(t), so consecutive steps' chains overlap; the post state
 //     passes between them in shared memory);
-//     twelve producer warps stage every row spiking at t -- its weights after
+//     fifteen producer warps stage every row spiking at t -- its weights after
 //     the potentiations it still owes from steps t - L .. t - 1 (silent since,
 //     a column spiked) -- into a per-parity ring of chunk buffers
 //     (full/empty mbarriers), then, once t's post spikes are out, store the
@@ -45,7 +45,7 @@
 // (sink_trace_kernel, [W][nPre]).
 constexpr int kSinkThreads = 640;
 constexpr int kSinkCols = 2;                      // post columns per sink block
-// producers: the warps off scheduler 0, where the chain warps (the step's
+// producers: the warps off scheduler 0 (15 of 20), where the chain warps (the step's
 // critical path) issue; a staged chunk is a row per producer
 constexpr int kSinkRows = kSinkThreads / 4 * 3;   // 384
 constexpr int kSinkLag = 4;                       // L: the background's lag in steps
