@@ -47,7 +47,7 @@ constexpr int kSinkThreads = 640;
 constexpr int kSinkCols = 2;                      // post columns per sink block
 // producers: the warps off scheduler 0 (15 of 20), where the chain warps (the step's
 // critical path) issue; a staged chunk is a row per producer
-constexpr int kSinkRows = kSinkThreads / 4 * 3;   // 384
+constexpr int kSinkRows = kSinkThreads / 4 * 3;   // 480
 constexpr int kSinkLag = 4;                       // L: the background's lag in steps
 constexpr int kTailMaxPost = 128;
 constexpr int kSinkMaxW = 256;                    // window steps (the sink blocks' spike history)
