@@ -198,3 +198,20 @@ def test_gpu_plastic_sink_odd_sizes_match_oracle(oracle_mod, n_kc, n_dn):
     p.sync()
     assert any(name.startswith("sink_step") for name, _, _ in p.kernel_stats())
     p.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("window", [1, 3, 7, 250])
+def test_gpu_plastic_sink_small_and_odd_windows_match_oracle(oracle_mod, window):
+    """Windows of 1, 3, 7 and 250 steps (the sink's step-parity rings, the
+    background's lag longer than the window) against the oracle."""
+    spec = specs.stdp_mbody_spec(2000, 60.0, a_plus=0.3)
+    gi = spec.group_index("kc_dn")
+    g = S.Simulation(spec, S.StorageMode.FromSpec, S.EngineOptions(window=window))
+    o = cpu_sim(oracle_mod, spec)
+    for n in (5, 17, 100, 478):
+        g.step(n)
+        o.step(n)
+        assert np.array_equal(g.group_weights("kc_dn"), o.group(gi)[1]), f"after {o.steps_done()} steps"
+    r, ro = g.finish(), o.finish()
+    assert np.array_equal(r.raster.step, ro[0]) and np.array_equal(r.raster.neuron, ro[2])
